@@ -1,0 +1,84 @@
+"""B200-native batched C2C FFT behind the reference ``stagefft`` plan/execute API.
+
+Hot path of arxiv 2203.09384 (SYCL-FFT): batched 1-D complex-to-complex
+power-of-two FFTs, N = 2..2048, single and double precision, forward and
+inverse.  ``make_plan`` / ``execute`` / ``execute_timed`` /
+``FourierTransformer`` keep the reference names and semantics
+(/root/reference/pkg/src/stagefft/__init__.py:70-123 for the hot-path subset)
+and run hand-written sm_100a CUDA kernels through the C ABI in
+``include/sfft.h``.  There is no CPU fallback.
+"""
+
+from .errors import (
+    ArgumentError,
+    CudaError,
+    DomainError,
+    FftError,
+    InsufficientDataError,
+    InvalidLengthError,
+    PlanError,
+    ShapeError,
+    UnsupportedLengthError,
+)
+from .executor import TimedExecution, execute, execute_timed, launch
+from .numerics import TABLE_MAX_LENGTH, TwiddleTable, build_twiddle_table, is_power_of_two, twiddle
+from .planner import (
+    ENGINE_MAX_LENGTH,
+    ENGINE_MIN_LENGTH,
+    SUPPORTED_LENGTHS,
+    SUPPORTED_RADICES,
+    Algorithm,
+    Direction,
+    FftPlan,
+    Precision,
+    digit_reversal_permutation,
+    factorize_stages,
+    make_plan,
+)
+from .sharding import execute_sharded, shard_bounds
+from .signalgen import KINDS, generate, generate_batch
+
+try:
+    from .estimator import FourierTransformer
+except ImportError:  # pragma: no cover - sklearn is optional for the kernel path
+    FourierTransformer = None
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Algorithm",
+    "ArgumentError",
+    "CudaError",
+    "Direction",
+    "DomainError",
+    "ENGINE_MAX_LENGTH",
+    "ENGINE_MIN_LENGTH",
+    "FftError",
+    "FftPlan",
+    "FourierTransformer",
+    "InsufficientDataError",
+    "InvalidLengthError",
+    "KINDS",
+    "PlanError",
+    "Precision",
+    "SUPPORTED_LENGTHS",
+    "SUPPORTED_RADICES",
+    "ShapeError",
+    "TABLE_MAX_LENGTH",
+    "TimedExecution",
+    "TwiddleTable",
+    "UnsupportedLengthError",
+    "build_twiddle_table",
+    "digit_reversal_permutation",
+    "execute",
+    "execute_sharded",
+    "execute_timed",
+    "factorize_stages",
+    "generate",
+    "generate_batch",
+    "is_power_of_two",
+    "launch",
+    "make_plan",
+    "shard_bounds",
+    "twiddle",
+]

@@ -1,0 +1,491 @@
+// C-ABI implementation: plan construction, twiddle tables, kernel dispatch,
+// and the host-buffer pipeline.  See include/sfft.h for the contract and the
+// reference interfaces each entry point replaces.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sfft.h"
+#include "sfft_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+using LaunchFn = cudaError_t (*)(const void* in, void* out, const void* tw, long long batch,
+                                 int* flag, cudaStream_t st);
+using PrepareFn = cudaError_t (*)();
+
+struct Variant {
+  int kernel;      // SFFT_KERNEL_*
+  int r;           // elements per thread (stockham R; tile: n)
+  int seq;         // sequences per CTA
+  int threads;     // threads per CTA
+  int smem;        // dynamic smem bytes
+  int passes;
+  int radices[8];
+  int tw_len;      // per-pass twiddle elements
+  LaunchFn launch[2];    // [direction]
+  PrepareFn prepare[2];  // [direction]
+};
+
+// ---------------------------------------------------------------- launchers
+template <typename T, int N, int R, int SEQ, bool INV>
+cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
+                            cudaStream_t st) {
+  using C = sfft::cx_t<T>;
+  constexpr int threads = (N / R) * SEQ;
+  constexpr int smem = SEQ * N * int(sizeof(C));
+  const long long grid = (batch + SEQ - 1) / SEQ;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  sfft::stockham_kernel<T, N, R, SEQ, INV><<<dim3(unsigned(grid)), threads, smem, st>>>(
+      static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
+  return cudaGetLastError();
+}
+template <typename T, int N, int R, int SEQ, bool INV>
+cudaError_t prepare_stockham() {
+  constexpr int smem = SEQ * N * int(sizeof(sfft::cx_t<T>));
+  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <typename T>
+constexpr int tile_smem(int n, int spt, int warps) {
+  return n * int(sizeof(sfft::cx_t<T>)) / 16 == 1 ? 0 : warps * 32 * spt * n * int(sizeof(sfft::cx_t<T>));
+}
+
+template <typename T, int N, int SPT, int W, bool INV>
+cudaError_t launch_tile(const void* in, void* out, const void*, long long batch, int* flag,
+                        cudaStream_t st) {
+  using C = sfft::cx_t<T>;
+  constexpr int smem = tile_smem<T>(N, SPT, W);
+  constexpr long long per_cta = 32LL * SPT * W;
+  const long long grid = (batch + per_cta - 1) / per_cta;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  sfft::tile_kernel<T, N, SPT, W, INV><<<dim3(unsigned(grid)), 32 * W, smem, st>>>(
+      static_cast<const C*>(in), static_cast<C*>(out), batch, flag);
+  return cudaGetLastError();
+}
+template <typename T, int N, int SPT, int W, bool INV>
+cudaError_t prepare_tile() {
+  constexpr int smem = tile_smem<T>(N, SPT, W);
+  return cudaFuncSetAttribute(sfft::tile_kernel<T, N, SPT, W, INV>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <typename T, int N, int R, int SEQ>
+Variant stockham_variant() {
+  Variant v{};
+  v.kernel = SFFT_KERNEL_STOCKHAM;
+  v.r = R;
+  v.seq = SEQ;
+  v.threads = (N / R) * SEQ;
+  v.smem = SEQ * N * int(sizeof(sfft::cx_t<T>));
+  v.passes = sfft::num_passes(N, R);
+  for (int p = 0; p < v.passes && p < 8; ++p) v.radices[p] = sfft::pass_radix(N, R, p);
+  v.tw_len = sfft::twiddle_table_len(N, R);
+  v.launch[0] = &launch_stockham<T, N, R, SEQ, false>;
+  v.launch[1] = &launch_stockham<T, N, R, SEQ, true>;
+  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false>;
+  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true>;
+  return v;
+}
+
+template <typename T, int N, int SPT, int W>
+Variant tile_variant() {
+  Variant v{};
+  v.kernel = SFFT_KERNEL_TILE;
+  v.r = N;
+  v.seq = 32 * SPT * W;
+  v.threads = 32 * W;
+  v.smem = tile_smem<T>(N, SPT, W);
+  v.passes = 1;
+  v.radices[0] = N;
+  v.tw_len = 0;
+  v.launch[0] = &launch_tile<T, N, SPT, W, false>;
+  v.launch[1] = &launch_tile<T, N, SPT, W, true>;
+  v.prepare[0] = &prepare_tile<T, N, SPT, W, false>;
+  v.prepare[1] = &prepare_tile<T, N, SPT, W, true>;
+  return v;
+}
+
+// Variant table, [precision][log2 n]; entry 0 is the planner's default.
+// Chosen so every CTA has 128-256 threads, every sequence is touched with
+// >= 32-byte contiguous segments per warp instruction, and the swizzled
+// exchanges are conflict-free (tests/test_bank_model.py).
+const std::vector<Variant>& variants(int precision, int log2n) {
+  static const std::vector<Variant> table[2][12] = {
+      {
+          {},
+          {tile_variant<float, 2, 8, 4>(), tile_variant<float, 2, 4, 8>()},
+          {tile_variant<float, 4, 4, 4>(), tile_variant<float, 4, 2, 8>()},
+          {tile_variant<float, 8, 4, 4>(), tile_variant<float, 8, 2, 4>()},
+          {tile_variant<float, 16, 2, 4>(), tile_variant<float, 16, 1, 8>()},
+          {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32>()},
+          {stockham_variant<float, 64, 8, 16>(), stockham_variant<float, 64, 16, 32>()},
+          {stockham_variant<float, 128, 8, 8>(), stockham_variant<float, 128, 16, 16>()},
+          {stockham_variant<float, 256, 16, 8>(), stockham_variant<float, 256, 8, 4>()},
+          {stockham_variant<float, 512, 16, 4>(), stockham_variant<float, 512, 8, 2>()},
+          {stockham_variant<float, 1024, 16, 2>(), stockham_variant<float, 1024, 8, 1>()},
+          {stockham_variant<float, 2048, 16, 1>(), stockham_variant<float, 2048, 8, 1>()},
+      },
+      {
+          {},
+          {tile_variant<double, 2, 4, 4>(), tile_variant<double, 2, 2, 8>()},
+          {tile_variant<double, 4, 2, 4>(), tile_variant<double, 4, 1, 8>()},
+          {tile_variant<double, 8, 1, 4>(), tile_variant<double, 8, 2, 4>()},
+          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64>()},
+          {stockham_variant<double, 32, 8, 32>(), stockham_variant<double, 32, 16, 64>()},
+          {stockham_variant<double, 64, 8, 16>(), stockham_variant<double, 64, 16, 32>()},
+          {stockham_variant<double, 128, 8, 8>(), stockham_variant<double, 128, 16, 16>()},
+          {stockham_variant<double, 256, 8, 4>(), stockham_variant<double, 256, 16, 8>()},
+          {stockham_variant<double, 512, 8, 2>(), stockham_variant<double, 512, 16, 4>()},
+          {stockham_variant<double, 1024, 8, 1>(), stockham_variant<double, 1024, 16, 2>()},
+          {stockham_variant<double, 2048, 16, 1>(), stockham_variant<double, 2048, 8, 1>()},
+      },
+  };
+  return table[precision][log2n];
+}
+
+bool is_pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+int log2i(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+// numerics.py:55-71: angle = (-2*pi/n)*k in double, cos + i*sin, factors[0] = 1.
+void base_table(int n, std::vector<double>& re, std::vector<double>& im) {
+  re.resize(n);
+  im.resize(n);
+  const double step = -2.0 * M_PI / double(n);
+  for (int k = 0; k < n; ++k) {
+    const double a = step * double(k);
+    re[k] = std::cos(a);
+    im[k] = std::sin(a);
+  }
+  re[0] = 1.0;
+  im[0] = 0.0;
+}
+
+void write_table(int precision, const std::vector<double>& re, const std::vector<double>& im,
+                 const std::vector<int>& idx, std::vector<unsigned char>& bytes) {
+  const size_t e = precision == SFFT_SINGLE ? 8 : 16;
+  bytes.resize(idx.size() * e);
+  for (size_t i = 0; i < idx.size(); ++i) {
+    if (precision == SFFT_SINGLE) {
+      const float v[2] = {float(re[idx[i]]), float(im[idx[i]])};  // rounded once
+      std::memcpy(bytes.data() + i * e, v, e);
+    } else {
+      const double v[2] = {re[idx[i]], im[idx[i]]};
+      std::memcpy(bytes.data() + i * e, v, e);
+    }
+  }
+}
+
+int check_length(int32_t n) {
+  if (!is_pow2(n))
+    return fail(SFFT_ERR_INVALID_LENGTH,
+                "transform length must be a power of two, got " + std::to_string(n));
+  if (n < SFFT_MIN_LENGTH || n > SFFT_MAX_LENGTH)
+    return fail(SFFT_ERR_UNSUPPORTED_LENGTH, "length " + std::to_string(n) +
+                                                 " outside supported range [2, 2048]");
+  return SFFT_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) {
+      err = cudaSetDevice(dev);
+      changed = err == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+constexpr int kHostStreams = 3;
+
+}  // namespace
+
+struct sfft_plan {
+  int32_t n = 0, precision = 0, direction = 0, device = 0, variant = 0;
+  int64_t batch = 0;
+  const Variant* v = nullptr;
+  void* d_tw = nullptr;
+  std::vector<unsigned char> host_base;  // base table in plan precision
+  // host-buffer pipeline state (lazily created, guarded by host_mu)
+  std::mutex host_mu;
+  bool host_ready = false;
+  int64_t host_chunk_rows = 0;
+  cudaStream_t streams[kHostStreams] = {};
+  void* d_in[kHostStreams] = {};
+  void* d_out[kHostStreams] = {};
+  int32_t* d_flag = nullptr;
+};
+
+extern "C" {
+
+int sfft_version(void) { return 100; /* 0.1.0 */ }
+
+const char* sfft_last_error(void) { return g_last_error.c_str(); }
+
+int sfft_num_variants(int32_t n, int32_t precision) {
+  if (!is_pow2(n) || n < SFFT_MIN_LENGTH || n > SFFT_MAX_LENGTH) return 0;
+  if (precision != SFFT_SINGLE && precision != SFFT_DOUBLE) return 0;
+  return int(variants(precision, log2i(n)).size());
+}
+
+int sfft_build_twiddle_table(int32_t n, int32_t precision, void* host_out, int64_t capacity) {
+  if (!is_pow2(n) || n > 4096)
+    return fail(SFFT_ERR_INVALID_LENGTH, "table length must be a power of two <= 4096");
+  if (precision != SFFT_SINGLE && precision != SFFT_DOUBLE)
+    return fail(SFFT_ERR_ARGUMENT, "precision must be SFFT_SINGLE or SFFT_DOUBLE");
+  const int64_t need = int64_t(n) * (precision == SFFT_SINGLE ? 8 : 16);
+  if (host_out == nullptr || capacity < need)
+    return fail(SFFT_ERR_ARGUMENT, "output buffer too small for twiddle table");
+  std::vector<double> re, im;
+  base_table(n, re, im);
+  std::vector<int> idx(n);
+  for (int k = 0; k < n; ++k) idx[k] = k;
+  std::vector<unsigned char> bytes;
+  write_table(precision, re, im, idx, bytes);
+  std::memcpy(host_out, bytes.data(), bytes.size());
+  return SFFT_OK;
+}
+
+int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int32_t direction,
+                             int64_t batch, int32_t device, int32_t variant) {
+  if (out == nullptr) return fail(SFFT_ERR_ARGUMENT, "plan out-pointer is NULL");
+  *out = nullptr;
+  if (int rc = check_length(n)) return rc;
+  if (precision != SFFT_SINGLE && precision != SFFT_DOUBLE)
+    return fail(SFFT_ERR_ARGUMENT, "precision must be SFFT_SINGLE or SFFT_DOUBLE");
+  if (direction != SFFT_FORWARD && direction != SFFT_INVERSE)
+    return fail(SFFT_ERR_ARGUMENT, "direction must be SFFT_FORWARD or SFFT_INVERSE");
+  if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
+  const auto& vs = variants(precision, log2i(n));
+  if (variant < 0 || variant >= int(vs.size()))
+    return fail(SFFT_ERR_PLAN, "kernel variant " + std::to_string(variant) + " does not exist");
+  if (device < 0) return fail(SFFT_ERR_ARGUMENT, "device must be >= 0");
+
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device >= ndev)
+    return fail(SFFT_ERR_CUDA, "device " + std::to_string(device) + " not present (" +
+                                   std::to_string(ndev) + " visible)");
+
+  sfft_plan* p = new (std::nothrow) sfft_plan();
+  if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "out of host memory");
+  p->n = n;
+  p->precision = precision;
+  p->direction = direction;
+  p->batch = batch;
+  p->device = device;
+  p->variant = variant;
+  p->v = &vs[variant];
+
+  std::vector<double> re, im;
+  base_table(n, re, im);
+  std::vector<int> idx(n);
+  for (int k = 0; k < n; ++k) idx[k] = k;
+  write_table(precision, re, im, idx, p->host_base);
+
+  // per-pass table: pass p >= 1, entry [(q-1)*L + k] = w_{L r}^{q k} = base[(n/(L r)) q k]
+  std::vector<int> tidx;
+  if (p->v->kernel == SFFT_KERNEL_STOCKHAM) {
+    int L = p->v->radices[0];
+    for (int pass = 1; pass < p->v->passes; ++pass) {
+      const int r = p->v->radices[pass];
+      const int step = n / (L * r);
+      for (int q = 1; q < r; ++q)
+        for (int k = 0; k < L; ++k) tidx.push_back(step * q * k);
+      L *= r;
+    }
+  }
+
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) {
+    delete p;
+    return cuda_fail(guard.err, "cudaSetDevice");
+  }
+  if (!tidx.empty()) {
+    std::vector<unsigned char> bytes;
+    write_table(precision, re, im, tidx, bytes);
+    e = cudaMalloc(&p->d_tw, bytes.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_tw, bytes.data(), bytes.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(p->d_tw);
+      delete p;
+      return cuda_fail(e, "twiddle upload");
+    }
+  }
+  e = p->v->prepare[direction]();
+  if (e != cudaSuccess) {
+    cudaFree(p->d_tw);
+    delete p;
+    return cuda_fail(e, "cudaFuncSetAttribute");
+  }
+  *out = p;
+  return SFFT_OK;
+}
+
+int sfft_plan_create(sfft_plan_t* out, int32_t n, int32_t precision, int32_t direction,
+                     int64_t batch, int32_t device) {
+  return sfft_plan_create_variant(out, n, precision, direction, batch, device, 0);
+}
+
+int sfft_plan_destroy(sfft_plan_t p) {
+  if (p == nullptr) return SFFT_OK;
+  {
+    DeviceGuard guard(p->device);
+    if (p->d_tw) cudaFree(p->d_tw);
+    if (p->host_ready) {
+      for (int i = 0; i < kHostStreams; ++i) {
+        cudaStreamSynchronize(p->streams[i]);
+        cudaFree(p->d_in[i]);
+        cudaFree(p->d_out[i]);
+        cudaStreamDestroy(p->streams[i]);
+      }
+      cudaFree(p->d_flag);
+    }
+  }
+  delete p;
+  return SFFT_OK;
+}
+
+int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
+  if (p == nullptr || info == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan or info");
+  std::memset(info, 0, sizeof(*info));
+  info->n = p->n;
+  info->precision = p->precision;
+  info->direction = p->direction;
+  info->device = p->device;
+  info->batch = p->batch;
+  info->kernel = p->v->kernel;
+  info->elems_per_thread = p->v->r;
+  info->seqs_per_cta = p->v->seq;
+  info->threads_per_cta = p->v->threads;
+  info->smem_bytes = p->v->smem;
+  info->num_passes = p->v->passes;
+  for (int i = 0; i < 8; ++i) info->radices[i] = p->v->radices[i];
+  info->twiddle_elems = p->v->tw_len;
+  info->variant = p->variant;
+  return SFFT_OK;
+}
+
+int sfft_plan_twiddles(sfft_plan_t p, void* host_out, int64_t capacity) {
+  if (p == nullptr || host_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL argument");
+  if (capacity < int64_t(p->host_base.size()))
+    return fail(SFFT_ERR_ARGUMENT, "output buffer too small for twiddle table");
+  std::memcpy(host_out, p->host_base.data(), p->host_base.size());
+  return SFFT_OK;
+}
+
+int sfft_execute(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                 int32_t* d_nonfinite) {
+  if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
+  if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
+  if (batch == 0) return SFFT_OK;
+  if (d_in == nullptr || d_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
+  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)
+    return fail(SFFT_ERR_ARGUMENT, "data pointers must be 16-byte aligned");
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  const cudaError_t e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch,
+                                                   reinterpret_cast<int*>(d_nonfinite),
+                                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return SFFT_OK;
+}
+
+int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch) {
+  if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
+  if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
+  if (batch == 0) return SFFT_OK;
+  if (h_in == nullptr || h_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
+  std::lock_guard<std::mutex> lock(p->host_mu);
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  const int64_t row_bytes = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
+  cudaError_t e = cudaSuccess;
+  if (!p->host_ready) {
+    for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i)
+      e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_flag, sizeof(int32_t) * kHostStreams);
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
+    p->host_ready = true;
+  }
+  // 16 MiB chunks: large enough for full-rate DMA, small enough to overlap
+  // copies in both directions with the kernels of neighbouring chunks.
+  // Staging buffers grow on demand, so small calls stay small.
+  const int64_t max_chunk_rows = (int64_t(16) << 20) / row_bytes > 0 ? (int64_t(16) << 20) / row_bytes : 1;
+  const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
+  if (want_rows > p->host_chunk_rows) {
+    for (int i = 0; i < kHostStreams; ++i) {
+      cudaStreamSynchronize(p->streams[i]);
+      cudaFree(p->d_in[i]);
+      cudaFree(p->d_out[i]);
+      p->d_in[i] = p->d_out[i] = nullptr;
+    }
+    p->host_chunk_rows = 0;
+    for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&p->d_in[i], want_rows * row_bytes);
+      if (e == cudaSuccess) e = cudaMalloc(&p->d_out[i], want_rows * row_bytes);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
+    p->host_chunk_rows = want_rows;
+  }
+  e = cudaMemsetAsync(p->d_flag, 0, sizeof(int32_t) * kHostStreams, p->streams[0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->streams[0]);
+  if (e != cudaSuccess) return cuda_fail(e, "flag reset");
+  const unsigned char* src = static_cast<const unsigned char*>(h_in);
+  unsigned char* dst = static_cast<unsigned char*>(h_out);
+  int chunk = 0;
+  for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
+    const int s = chunk % kHostStreams;
+    const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
+    const size_t bytes = size_t(rows * row_bytes);
+    cudaStream_t st = p->streams[s];
+    e = cudaMemcpyAsync(p->d_in[s], src + row * row_bytes, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, st);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    e = cudaMemcpyAsync(dst + row * row_bytes, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  int32_t flags[kHostStreams] = {};
+  for (int i = 0; i < kHostStreams; ++i) {
+    e = cudaStreamSynchronize(p->streams[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  }
+  e = cudaMemcpy(flags, p->d_flag, sizeof(flags), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "flag read");
+  for (int i = 0; i < kHostStreams; ++i)
+    if (flags[i]) return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
+  return SFFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// Device primitives for the batched C2C FFT: complex arithmetic, compile-time
+// twiddles and fully unrolled in-register DFTs.
+//
+// Replaces the per-stage numpy arithmetic of the reference butterfly engine:
+//   kernels.py:98-104  (_dft4: radix-4 DFT with rot = -i)
+//   kernels.py:126-151 (radix8_stage: two DFT-4s + eighth-root constants)
+// Here a radix-r DFT (r <= 32) is a radix-2 decision-in-frequency network over
+// r registers; every twiddle inside it is a compile-time constant, and the
+// +-1, +-i and (+-1 +- i)/sqrt(2) factors are strength-reduced exactly like the
+// reference's radix-8 constants (kernels.py:136-141).  Only forward kernels
+// exist; the inverse uses IDFT(x) = swap(DFT(swap(x))) with swap(a+bi) = b+ai,
+// which is exact, so "conjugate twiddles" (kernels.py:70-71) costs nothing.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+#include <utility>
+
+namespace sfft {
+
+template <typename T> struct CxOf;
+template <> struct CxOf<float> { using type = float2; };
+template <> struct CxOf<double> { using type = double2; };
+template <typename T> using cx_t = typename CxOf<T>::type;
+
+// ---------------------------------------------------------------- static_for
+template <int I, int END, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < END) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, END>(f);
+  }
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+
+__host__ __device__ constexpr int bitrev(int k, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((k >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// cos(2*pi*j/32), j in [0, 32), correctly rounded doubles (50-digit reference).
+__host__ __device__ constexpr double cos32(int j) {
+  j &= 31;
+  if (j > 16) j = 32 - j;  // cos is even
+  bool neg = false;
+  if (j > 8) { j = 16 - j; neg = true; }  // cos(pi - x) = -cos(x)
+  double c = 0.0;
+  switch (j) {
+    case 0: c = 1.0; break;
+    case 1: c = 0.9807852804032304; break;
+    case 2: c = 0.9238795325112867; break;
+    case 3: c = 0.8314696123025452; break;
+    case 4: c = 0.7071067811865476; break;
+    case 5: c = 0.5555702330196022; break;
+    case 6: c = 0.3826834323650898; break;
+    case 7: c = 0.19509032201612828; break;
+    default: c = 0.0; break;
+  }
+  return neg ? -c : c;
+}
+__host__ __device__ constexpr double sin32(int j) { return cos32(8 - j + 32); }
+
+// ------------------------------------------------------------ complex helpers
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return C{a.x + b.x, a.y + b.y}; }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return C{a.x - b.x, a.y - b.y}; }
+template <typename C> __device__ __forceinline__ C cmul(C a, C w) {
+  return C{a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
+}
+template <typename C> __device__ __forceinline__ C cswap(C a) { return C{a.y, a.x}; }
+
+// a * exp(-2*pi*i*J/L) with J, L compile-time, L a power of two <= 32.
+template <int J, int L, typename C>
+__device__ __forceinline__ C twiddle_const(C a) {
+  using T = decltype(a.x);
+  constexpr int j = ((J % L) + L) % L;
+  constexpr T h = T(0.7071067811865476);
+  if constexpr (j == 0) {
+    return a;
+  } else if constexpr (2 * j == L) {
+    return C{-a.x, -a.y};
+  } else if constexpr (4 * j == L) {  // -i
+    return C{a.y, -a.x};
+  } else if constexpr (4 * j == 3 * L) {  // +i
+    return C{-a.y, a.x};
+  } else if constexpr (8 * j == L) {  // (1 - i)/sqrt2
+    return C{(a.x + a.y) * h, (a.y - a.x) * h};
+  } else if constexpr (8 * j == 3 * L) {  // (-1 - i)/sqrt2
+    return C{(a.y - a.x) * h, -(a.x + a.y) * h};
+  } else if constexpr (8 * j == 5 * L) {  // (-1 + i)/sqrt2
+    return C{-(a.x + a.y) * h, (a.x - a.y) * h};
+  } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
+    return C{(a.x - a.y) * h, (a.x + a.y) * h};
+  } else {
+    constexpr int j32 = j * (32 / L);
+    constexpr T c = T(cos32(j32));
+    constexpr T s = T(-sin32(j32));
+    return cmul(a, C{c, s});
+  }
+}
+
+// In-place forward DFT of R registers, natural order in and out.
+template <int R, typename C>
+__device__ __forceinline__ void dft_regs(C (&v)[R]) {
+  static_assert((R & (R - 1)) == 0 && R >= 1 && R <= 32, "radix");
+  if constexpr (R == 1) {
+    return;
+  } else {
+    constexpr int LOG = ilog2(R);
+    static_for<0, LOG>([&](auto S) {
+      constexpr int len = R >> decltype(S)::value;
+      constexpr int half = len / 2;
+      static_for<0, R / len>([&](auto B) {
+        static_for<0, half>([&](auto J) {
+          constexpr int ia = decltype(B)::value * len + decltype(J)::value;
+          constexpr int ib = ia + half;
+          const C a = v[ia];
+          const C b = v[ib];
+          v[ia] = cadd(a, b);
+          v[ib] = twiddle_const<decltype(J)::value, len>(csub(a, b));
+        });
+      });
+    });
+    C t[R];
+    static_for<0, R>([&](auto K) { t[decltype(K)::value] = v[bitrev(decltype(K)::value, LOG)]; });
+    static_for<0, R>([&](auto K) { v[decltype(K)::value] = t[decltype(K)::value]; });
+  }
+}
+
+// ----------------------------------------------------- global memory streams
+// Streaming (evict-first) accesses: every element is read once and written once.
+__device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+
+// Non-finite detection (executor.py:72-73 raises DomainError on NaN/Inf
+// input).  The kernels OR a sticky bit per thread and publish it once.
+__device__ __forceinline__ uint32_t nonfinite_bits(float2 v) {
+  const uint32_t a = __float_as_uint(v.x) & 0x7f800000u;
+  const uint32_t b = __float_as_uint(v.y) & 0x7f800000u;
+  return (a == 0x7f800000u) | (b == 0x7f800000u);
+}
+__device__ __forceinline__ uint32_t nonfinite_bits(double2 v) {
+  const uint32_t a = uint32_t(__double2hiint(v.x)) & 0x7ff00000u;
+  const uint32_t b = uint32_t(__double2hiint(v.y)) & 0x7ff00000u;
+  return (a == 0x7ff00000u) | (b == 0x7ff00000u);
+}
+
+template <typename C, typename T>
+__device__ __forceinline__ C cscale(C a, T s) { return C{a.x * s, a.y * s}; }
+
+}  // namespace sfft

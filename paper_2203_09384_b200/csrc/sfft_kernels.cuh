@@ -1,0 +1,316 @@
+// Batched C2C FFT kernels for sm_100a.
+//
+// Two kernel families cover N = 2 .. 2048 in fp32 and fp64:
+//
+// * stockham_kernel  (N >= 64 fp32, N >= 32 fp64)
+//   G = N/R threads own one sequence; each thread keeps R elements in
+//   registers.  Pass 0 loads straight from HBM (lane j reads x[j + m*G]:
+//   consecutive lanes, consecutive addresses), every pass is a radix-r DFT in
+//   registers with per-pass twiddles from the plan's table, the exchange
+//   between passes goes through XOR-swizzled (bank-conflict-free) shared
+//   memory, and the last pass writes straight to HBM in natural order
+//   (Stockham autosort: no digit-reversal gather, cf. executor.py:77).
+//   One HBM read + one HBM write per element.
+//
+// * tile_kernel      (N <= 32 fp32, N <= 16 fp64)
+//   One thread owns whole sequences.  A warp stages a contiguous tile of
+//   32*SPT sequences into swizzled shared memory with 16-byte cp.async
+//   (fully coalesced, asynchronous), each thread runs its length-N DFT in
+//   registers with compile-time twiddles, and the warp streams the tile back
+//   with 16-byte coalesced stores.  fp32 N = 2 (one 16-byte chunk per
+//   sequence) skips the staging altogether.
+//
+// Both fuse: the inverse direction (swap trick), the 1/N inverse scale
+// (executor.py:93-94; exact for powers of two) and the non-finite input
+// check (executor.py:72-73) into the single pass over HBM.
+#pragma once
+
+#include "sfft_device.cuh"
+
+namespace sfft {
+
+// ------------------------------------------------------------ pass schedule
+// N = r0 * R^(P-1) with the (smaller) remainder radix r0 first: pass 0 has
+// stride 1 and therefore needs no twiddles at all.
+__host__ __device__ constexpr int remainder_radix(int n, int r) {
+  while (n % r == 0 && n > 1) n /= r;
+  return n;
+}
+__host__ __device__ constexpr int num_passes(int n, int r) {
+  int p = 0;
+  int m = n;
+  while (m % r == 0 && m > 1) { m /= r; ++p; }
+  return p + (m > 1 ? 1 : 0);
+}
+__host__ __device__ constexpr int pass_radix(int n, int r, int p) {
+  return (remainder_radix(n, r) > 1 && p == 0) ? remainder_radix(n, r) : r;
+}
+__host__ __device__ constexpr int pass_stride(int n, int r, int p) {
+  int l = 1;
+  for (int i = 0; i < p; ++i) l *= pass_radix(n, r, i);
+  return l;
+}
+// offset (in elements) of pass p's twiddles in the per-pass table:
+// pass p >= 1 stores (r_p - 1) * L_p entries, [(q-1)*L + k] = w_{L r}^{q k}.
+__host__ __device__ constexpr int pass_twiddle_offset(int n, int r, int p) {
+  int off = 0;
+  for (int i = 1; i < p; ++i) off += (pass_radix(n, r, i) - 1) * pass_stride(n, r, i);
+  return off;
+}
+__host__ __device__ constexpr int twiddle_table_len(int n, int r) {
+  return pass_twiddle_offset(n, r, num_passes(n, r));
+}
+
+// --------------------------------------------------------- smem swizzles
+// Element-granular XOR swizzle: 128-byte bank rows hold 16 fp32 complex or
+// 8 fp64 complex; two XOR terms make every Stockham read and write pattern
+// of the configured (N, R) pairs conflict-free (tests/test_bank_model.py
+// checks this with a bank model).
+template <typename T>
+__device__ __forceinline__ int swz_elem(int e) {
+  if constexpr (sizeof(T) == 4) {
+    return e ^ (((e >> 4) ^ (e >> 8)) & 15);
+  } else {
+    return e ^ (((e >> 3) ^ (e >> 6)) & 7);
+  }
+}
+// 16-byte-chunk swizzle for the tile kernel (8 chunks per bank row).
+__device__ __forceinline__ int swz_chunk(int c) { return c ^ (((c >> 3) ^ (c >> 6)) & 7); }
+
+template <int G>
+__device__ __forceinline__ void seq_sync(int s) {
+  if constexpr (G <= 32) {
+    __syncwarp();
+  } else {
+    // named barrier per sequence: only the G threads of one sequence wait
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(G) : "memory");
+  }
+}
+
+// ---------------------------------------------------------- Stockham kernel
+template <typename T, int N, int R, int SEQ, bool INV>
+__global__ void __launch_bounds__((N / R) * SEQ)
+stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
+                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  constexpr int G = N / R;
+  constexpr int NP = num_passes(N, R);
+  static_assert(G >= 1 && (N % R) == 0, "geometry");
+  static_assert(G <= 32 || SEQ <= 15, "named barrier ids");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int s = tid / G;
+  const int j = tid - s * G;
+  const long long seq = (long long)blockIdx.x * SEQ + s;
+  const bool valid = seq < batch;
+  const int sbase = s * N;
+
+  C v[R];
+  if (valid) {
+    const C* src = in + seq * N + j;
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+  } else {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
+  }
+  if (nonfinite != nullptr) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int m = 0; m < R; ++m) bad |= nonfinite_bits(v[m]);
+    if (bad) atomicOr(nonfinite, 1);
+  }
+  if constexpr (INV) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
+  }
+
+  static_for<0, NP>([&](auto P) {
+    constexpr int p = decltype(P)::value;
+    constexpr int r = pass_radix(N, R, p);
+    constexpr int L = pass_stride(N, R, p);
+    constexpr int NB = R / r;  // butterflies per thread in this pass
+    if constexpr (p > 0) {
+      // gather this pass's inputs x[j + m*G] from the exchange buffer
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = sm[swz_elem<T>(sbase + j + m * G)];
+      // twiddles w_{L r}^{q k}, k = b mod L  (kernels.py:41-72, gathered
+      // from the plan table instead of rebuilt per call)
+      const C* twp = tw + pass_twiddle_offset(N, R, p);
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int k = (j + t * G) & (L - 1);
+#pragma unroll
+        for (int q = 1; q < r; ++q) {
+          v[t + q * NB] = cmul(v[t + q * NB], __ldg(twp + (q - 1) * L + k));
+        }
+      }
+    }
+    // radix-r DFTs in registers
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      C u[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) u[q] = v[t + q * NB];
+      dft_regs<r>(u);
+#pragma unroll
+      for (int q = 0; q < r; ++q) v[t + q * NB] = u[q];
+    }
+    if constexpr (p == NP - 1) {
+      // last pass: output index b + q*L == j + m*G -> coalesced store
+      if (valid) {
+        C* dst = out + seq * N + j;
+        constexpr T scale = INV ? T(1) / T(N) : T(1);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+          C y = v[m];
+          if constexpr (INV) y = cscale(cswap(y), scale);
+          st_stream(dst + m * G, y);
+        }
+      }
+    } else {
+      if constexpr (p > 0) seq_sync<G>(s);  // everyone has read before we overwrite
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int b = j + t * G;
+        const int k = b & (L - 1);
+        const int base = (b - k) * r + k;
+#pragma unroll
+        for (int q = 0; q < r; ++q) sm[swz_elem<T>(sbase + base + q * L)] = v[t + q * NB];
+      }
+      seq_sync<G>(s);
+    }
+  });
+}
+
+// -------------------------------------------------------------- tile kernel
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <typename C>
+__device__ __forceinline__ void chunk_to_cx(float4 f, C* dst);
+template <>
+__device__ __forceinline__ void chunk_to_cx<float2>(float4 f, float2* dst) {
+  dst[0] = make_float2(f.x, f.y);
+  dst[1] = make_float2(f.z, f.w);
+}
+template <>
+__device__ __forceinline__ void chunk_to_cx<double2>(float4 f, double2* dst) {
+  dst[0] = *reinterpret_cast<const double2*>(&f);
+}
+template <typename C>
+__device__ __forceinline__ float4 cx_to_chunk(const C* src);
+template <>
+__device__ __forceinline__ float4 cx_to_chunk<float2>(const float2* src) {
+  return make_float4(src[0].x, src[0].y, src[1].x, src[1].y);
+}
+template <>
+__device__ __forceinline__ float4 cx_to_chunk<double2>(const double2* src) {
+  return *reinterpret_cast<const float4*>(src);
+}
+
+template <typename T, int N, bool INV>
+__device__ __forceinline__ void seq_dft(cx_t<T> (&x)[N], uint32_t& bad, bool check) {
+  if (check) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) bad |= nonfinite_bits(x[i]);
+  }
+  if constexpr (INV) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = cswap(x[i]);
+  }
+  dft_regs<N>(x);
+  if constexpr (INV) {
+    constexpr T scale = T(1) / T(N);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = cscale(cswap(x[i]), scale);
+  }
+}
+
+template <typename T, int N, int SPT, int WARPS, bool INV>
+__global__ void __launch_bounds__(32 * WARPS)
+tile_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out, long long batch,
+            int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  constexpr int E = sizeof(C);
+  constexpr int EPC = 16 / E;         // elements per 16-byte chunk
+  constexpr int K = N / EPC;          // chunks per sequence
+  static_assert(K >= 1 && N % EPC == 0, "tile geometry");
+  constexpr int TILE_CH = 32 * SPT * K;  // chunks per warp tile
+  constexpr int CPL = SPT * K;           // chunks per lane
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const long long tile = (long long)blockIdx.x * WARPS + warp;
+  const long long total_ch = batch * K;
+  const long long ch0 = tile * TILE_CH;
+  const float4* gin = reinterpret_cast<const float4*>(in);
+  float4* gout = reinterpret_cast<float4*>(out);
+  const bool check = nonfinite != nullptr;
+  uint32_t bad = 0;
+
+  if constexpr (K == 1) {
+    // one chunk == one sequence: no staging
+    float4 f[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const long long c = ch0 + lane + 32 * i;
+      f[i] = c < total_ch ? ld_stream(gin + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      C x[N];
+      chunk_to_cx<C>(f[i], x);
+      seq_dft<T, N, INV>(x, bad, check);
+      f[i] = cx_to_chunk<C>(x);
+    }
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const long long c = ch0 + lane + 32 * i;
+      if (c < total_ch) st_stream(gout + c, f[i]);
+    }
+  } else {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4* ws = reinterpret_cast<float4*>(smem_raw) + warp * TILE_CH;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane + 32 * i;
+      const long long gc = ch0 + c;
+      if (gc < total_ch) {
+        cp_async16(ws + swz_chunk(c), gin + gc);
+      } else {
+        ws[swz_chunk(c)] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+#pragma unroll 1
+    for (int u = 0; u < SPT; ++u) {
+      const int q = u * 32 + lane;  // sequence within the tile
+      C x[N];
+#pragma unroll
+      for (int c = 0; c < K; ++c) chunk_to_cx<C>(ws[swz_chunk(q * K + c)], x + c * EPC);
+      seq_dft<T, N, INV>(x, bad, check);
+#pragma unroll
+      for (int c = 0; c < K; ++c) ws[swz_chunk(q * K + c)] = cx_to_chunk<C>(x + c * EPC);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane + 32 * i;
+      const long long gc = ch0 + c;
+      if (gc < total_ch) st_stream(gout + gc, ws[swz_chunk(c)]);
+    }
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+
+}  // namespace sfft

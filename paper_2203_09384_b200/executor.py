@@ -1,0 +1,176 @@
+"""Batched plan execution on the GPU (mirror of executor.py:1-96).
+
+``execute(plan, signal)`` keeps the reference contract -- the input is never
+written, the output is fresh memory, repeated runs are bit-identical, one plan
+may be shared by many threads -- and widens it:
+
+* ``signal`` may be 1-D ``(N,)`` (reference behaviour) or batched ``(B, N)``;
+  anything else, or a last axis != plan length, is a ``ShapeError``
+  (executor.py:64-69);
+* numpy / array-like input runs through the native host pipeline
+  (``sfft_execute_host``: chunked H2D -> kernel -> D2H) and returns numpy;
+  a torch CUDA tensor stays on its device (``sfft_execute`` on the current
+  stream) and returns a tensor there.
+
+Every path launches the sm_100a kernels; there is no CPU fallback.  NaN/Inf
+input raises ``DomainError`` (executor.py:72-73) -- detected inside the kernel
+while it loads the data, so validation costs no extra pass over memory.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _native
+from .errors import DomainError, InvalidLengthError, ShapeError
+from .planner import FftPlan
+
+try:  # torch is the device-memory/stream plumbing; numpy input works without it
+    import torch
+except ImportError:  # pragma: no cover - torch is in the image
+    torch = None
+
+
+class TimedExecution(NamedTuple):
+    """executor.py:28-31: output plus host dispatch and device compute time."""
+
+    output: object
+    dispatch_us: float
+    compute_us: float
+
+
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _check_shape(plan: FftPlan, shape) -> int:
+    if len(shape) not in (1, 2):
+        raise ShapeError(f"signal must be (N,) or (batch, N), got shape {tuple(shape)}")
+    if shape[-1] != plan.length:
+        raise ShapeError(f"signal length {shape[-1]} does not match plan length {plan.length}")
+    rows = 1 if len(shape) == 1 else int(shape[0])
+    if rows == 0:
+        raise InvalidLengthError(f"signal batch is empty, shape {tuple(shape)}")
+    if plan.batch is not None and len(shape) == 2 and rows != plan.batch:
+        raise ShapeError(f"signal has {rows} rows; the plan was made for batch={plan.batch}")
+    return rows
+
+
+def _default_device(plan: FftPlan) -> int:
+    if plan.device is not None:
+        return plan.device
+    if torch is not None and torch.cuda.is_available():
+        return torch.cuda.current_device()
+    return 0
+
+
+# ----------------------------------------------------------------- numpy path
+def _prepare_host(plan: FftPlan, signal):
+    x = np.asarray(signal)
+    rows = _check_shape(plan, x.shape)
+    if x.dtype.kind not in "fciu":
+        raise DomainError(f"signal has non-numeric dtype {x.dtype}")
+    # complex128 -> complex64 for a single-precision plan, as validation.py:26 does
+    xc = np.ascontiguousarray(x, dtype=plan.dtype)
+    if xc.ctypes.data % 16:
+        xc = xc.copy()
+    return x, xc, rows
+
+
+def _execute_host(plan: FftPlan, signal):
+    x, xc, rows = _prepare_host(plan, signal)
+    out = np.empty(xc.shape, dtype=plan.dtype)
+    handle = plan.native_handle(_default_device(plan))
+    _native.check(_native.lib().sfft_execute_host(handle, xc.ctypes.data, out.ctypes.data, rows))
+    return out
+
+
+# ----------------------------------------------------------------- torch path
+def _prepare_device(plan: FftPlan, x):
+    rows = _check_shape(plan, tuple(x.shape))
+    if x.dtype == torch.bool:  # numpy kind "b" is rejected too (executor.py:70-71)
+        raise DomainError(f"signal has non-numeric dtype {x.dtype}")
+    want = torch.complex64 if plan.dtype == np.complex64 else torch.complex128
+    xc = x.to(want).contiguous()
+    if xc.data_ptr() % 16:
+        xc = xc.clone()
+    return xc, rows
+
+
+def launch(plan: FftPlan, x_in, x_out, rows: int, *, stream=None, flag=None) -> None:
+    """Asynchronous launch on device tensors (no validation, no sync).
+
+    ``x_in``/``x_out`` are contiguous CUDA tensors of the plan dtype holding
+    ``rows`` sequences; ``flag`` an int32 CUDA tensor the kernel ORs 1 into on
+    NaN/Inf input.  This is the call ``bench.py`` times.
+    """
+    dev = x_in.device.index
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    handle = plan.native_handle(dev)
+    _native.check(
+        _native.lib().sfft_execute(
+            handle,
+            ctypes.c_void_p(x_in.data_ptr()),
+            ctypes.c_void_p(x_out.data_ptr()),
+            rows,
+            ctypes.c_void_p(stream.cuda_stream),
+            None if flag is None else ctypes.c_void_p(flag.data_ptr()),
+        )
+    )
+
+
+def _execute_device(plan: FftPlan, x, timed: bool = False):
+    t0 = time.perf_counter_ns()
+    xc, rows = _prepare_device(plan, x)
+    out = torch.empty_like(xc)
+    flag = torch.zeros(1, dtype=torch.int32, device=xc.device)
+    stream = torch.cuda.current_stream(xc.device)
+    if timed:
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+    t1 = time.perf_counter_ns()
+    launch(plan, xc, out, rows, stream=stream, flag=flag)
+    if timed:
+        stop.record(stream)
+    if int(flag.item()):  # synchronises the stream
+        raise DomainError("signal contains NaN or Inf values")
+    compute_us = start.elapsed_time(stop) * 1000.0 if timed else 0.0
+    return out, (t1 - t0) / 1000.0, compute_us
+
+
+# ----------------------------------------------------------------- public API
+def execute(plan: FftPlan, signal):
+    """Run ``plan`` on ``signal`` and return fresh output (executor.py:50-52)."""
+    if _is_torch(signal):
+        if signal.is_cuda:
+            return _execute_device(plan, signal)[0]
+        return torch.from_numpy(_execute_host(plan, signal.numpy()))
+    return _execute_host(plan, signal)
+
+
+def execute_timed(plan: FftPlan, signal) -> TimedExecution:
+    """execute plus timing (executor.py:55-96).
+
+    ``dispatch_us``: host time from entry to the kernel launch (validation,
+    dtype conversion and, for host input, the H2D copy); ``compute_us``: the
+    kernel's device time from CUDA events on the launch stream.
+    """
+    if _is_torch(signal) and signal.is_cuda:
+        return TimedExecution(*_execute_device(plan, signal, timed=True))
+    t0 = time.perf_counter_ns()
+    host = signal.numpy() if _is_torch(signal) else signal
+    x, xc, _ = _prepare_host(plan, host)
+    dev = _default_device(plan)
+    xd = torch.from_numpy(xc).to(f"cuda:{dev}")
+    t_h2d = time.perf_counter_ns()
+    out_d, dispatch_us, compute_us = _execute_device(plan, xd, timed=True)
+    out = out_d.cpu().numpy()
+    if _is_torch(signal):
+        out = torch.from_numpy(out)
+    return TimedExecution(out, (t_h2d - t0) / 1000.0 + dispatch_us, compute_us)
