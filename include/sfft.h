@@ -86,6 +86,10 @@ int sfft_num_variants(int32_t n, int32_t precision);
 int sfft_build_twiddle_table(int32_t n, int32_t precision, void* host_out,
                              int64_t capacity_bytes);
 
+/* Geometry of kernel variant `variant` for (n, precision) without creating a
+ * plan or touching a device (direction/device/batch fields are zero). */
+int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_info_t* info);
+
 /* make_plan: validate (n power of two in [2, 2048]), choose the kernel,
  * build the twiddle table in double (rounded once for single), upload the
  * per-pass table to `device`.  batch >= 0 (0 = unspecified). */

@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = (
     "sfft_plan_create_variant",
     "sfft_plan_destroy",
     "sfft_plan_info",
+    "sfft_variant_info",
     "sfft_plan_twiddles",
     "sfft_execute",
     "sfft_execute_host",
@@ -79,6 +80,7 @@ def _bind(lib):
         "sfft_plan_destroy": ([p], ctypes.c_int),
         "sfft_plan_info": ([p, ctypes.POINTER(PlanInfo)], ctypes.c_int),
         "sfft_plan_twiddles": ([p, p, i64], ctypes.c_int),
+        "sfft_variant_info": ([i32, i32, i32, ctypes.POINTER(PlanInfo)], ctypes.c_int),
         "sfft_execute": ([p, p, p, i64, p, p], ctypes.c_int),
         "sfft_execute_host": ([p, p, p, i64], ctypes.c_int),
         "sfft_last_error": ([], ctypes.c_char_p),
@@ -104,6 +106,13 @@ def lib():
                     )
                 _lib = _bind(ctypes.CDLL(LIB_PATH))
     return _lib
+
+
+def variant_info(n: int, precision_code: int, variant: int = 0) -> dict:
+    """Kernel geometry of a variant, host-only (sfft_variant_info)."""
+    info = PlanInfo()
+    check(lib().sfft_variant_info(n, precision_code, variant, ctypes.byref(info)))
+    return info.as_dict()
 
 
 def check(status: int) -> None:

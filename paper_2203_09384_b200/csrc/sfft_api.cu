@@ -396,6 +396,30 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   return SFFT_OK;
 }
 
+int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_info_t* info) {
+  if (info == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL info");
+  if (int rc = check_length(n)) return rc;
+  if (precision != SFFT_SINGLE && precision != SFFT_DOUBLE)
+    return fail(SFFT_ERR_ARGUMENT, "precision must be SFFT_SINGLE or SFFT_DOUBLE");
+  const auto& vs = variants(precision, log2i(n));
+  if (variant < 0 || variant >= int(vs.size()))
+    return fail(SFFT_ERR_PLAN, "kernel variant " + std::to_string(variant) + " does not exist");
+  const Variant& v = vs[variant];
+  std::memset(info, 0, sizeof(*info));
+  info->n = n;
+  info->precision = precision;
+  info->kernel = v.kernel;
+  info->elems_per_thread = v.r;
+  info->seqs_per_cta = v.seq;
+  info->threads_per_cta = v.threads;
+  info->smem_bytes = v.smem;
+  info->num_passes = v.passes;
+  for (int i = 0; i < 8; ++i) info->radices[i] = v.radices[i];
+  info->twiddle_elems = v.tw_len;
+  info->variant = variant;
+  return SFFT_OK;
+}
+
 int sfft_plan_twiddles(sfft_plan_t p, void* host_out, int64_t capacity) {
   if (p == nullptr || host_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL argument");
   if (capacity < int64_t(p->host_base.size()))

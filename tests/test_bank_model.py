@@ -1,0 +1,121 @@
+"""Shared-memory bank model of the kernels' exchange patterns (CPU only).
+
+Re-derives, for every compiled kernel variant (queried from the library with
+sfft_variant_info), the addresses each warp instruction touches in shared
+memory -- the Stockham scatter/gather of csrc/sfft_kernels.cuh with its XOR
+swizzle, and the tile kernel's 16-byte chunk staging -- and counts
+bank-conflict wavefronts with the 32 x 4-byte bank model.  The default
+variant of every (precision, N) must be conflict-free; ncu's
+l1tex__data_bank_conflicts_pipe_lsu_mem_shared counters confirm it on the GPU.
+"""
+
+import pytest
+
+from paper_2203_09384_b200 import _native
+
+ALL_N = [2**p for p in range(1, 12)]
+
+
+def swz_elem(e: int, esize: int) -> int:
+    if esize == 8:
+        return e ^ (((e >> 4) ^ (e >> 8)) & 15)
+    return e ^ (((e >> 3) ^ (e >> 6)) & 7)
+
+
+def swz_chunk(c: int) -> int:
+    return c ^ (((c >> 3) ^ (c >> 6)) & 7)
+
+
+def wavefronts(unit_idx, unit_bytes):
+    """(actual, ideal) wavefronts for one warp instruction; unit_idx per lane."""
+    words = set()
+    for u in unit_idx:
+        for w in range(unit_bytes // 4):
+            words.add(u * (unit_bytes // 4) + w)
+    banks = {}
+    for w in words:
+        banks.setdefault(w % 32, set()).add(w)
+    return max(len(v) for v in banks.values()), max(1, len(words) // 32)
+
+
+def stockham_instructions(n, r, esize):
+    g = n // r
+    radices = []
+    m = n
+    p = 0
+    while m % r == 0 and m > 1:
+        m //= r
+        p += 1
+    radices = ([m] if m > 1 else []) + [r] * p
+    lanes = [(lane // g, lane % g) if g < 32 else (0, lane) for lane in range(32)]
+    out = []
+    stride = 1
+    for pi, rad in enumerate(radices):
+        nb = r // rad
+        if pi > 0:  # gather x[j + m*G]
+            for mm in range(r):
+                out.append([swz_elem(s * n + j + mm * g, esize) for s, j in lanes])
+        if pi < len(radices) - 1:  # scatter to Stockham destination
+            for t in range(nb):
+                for q in range(rad):
+                    idx = []
+                    for s, j in lanes:
+                        b = j + t * g
+                        k = b % stride
+                        idx.append(swz_elem(s * n + (b - k) * rad + k + q * stride, esize))
+                    out.append(idx)
+        stride *= rad
+    return out
+
+
+def tile_instructions(n, spt, esize):
+    k = n * esize // 16
+    if k == 1:
+        return []  # no staging
+    out = []
+    for i in range(spt * k):  # cp.async / coalesced chunk accesses
+        out.append([swz_chunk(lane + 32 * i) for lane in range(32)])
+    for u in range(spt):  # per-thread sequence accesses
+        for c in range(k):
+            out.append([swz_chunk((u * 32 + lane) * k + c) for lane in range(32)])
+    return out
+
+
+def conflict_ratio(info, esize):
+    if info["kernel"] == _native.SFFT_KERNEL_STOCKHAM:
+        instrs = stockham_instructions(info["n"], info["elems_per_thread"], esize)
+        unit = esize
+    else:
+        spt = info["seqs_per_cta"] // info["threads_per_cta"]
+        instrs = tile_instructions(info["n"], spt, esize)
+        unit = 16
+    if not instrs:
+        return 1.0
+    tot = ideal = 0
+    for idx in instrs:
+        a, b = wavefronts(idx, unit)
+        tot += a
+        ideal += b
+    return tot / ideal
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("n", ALL_N)
+def test_default_variant_conflict_free(n, prec):
+    info = _native.variant_info(n, prec, 0)
+    assert conflict_ratio(info, 8 if prec == 0 else 16) == 1.0
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("n", ALL_N)
+def test_every_variant_bounded(n, prec):
+    lib = _native.lib()
+    for v in range(lib.sfft_num_variants(n, prec)):
+        info = _native.variant_info(n, prec, v)
+        assert conflict_ratio(info, 8 if prec == 0 else 16) <= 1.5
+
+
+def test_swizzles_are_bijections():
+    for esize in (8, 16):
+        assert sorted(swz_elem(e, esize) for e in range(4096)) == list(range(4096))
+    assert sorted(swz_chunk(c) for c in range(4096)) == list(range(4096))
