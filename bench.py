@@ -1,0 +1,434 @@
+"""Benchmark: batched C2C FFT on B200 vs the reference CPU path.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line.  A step is one batched execute over the whole workload.  Default
+workload = BASELINE.json configs[1]: fp32 forward C2C, N=1024, batch=65536
+(512 MiB in + 512 MiB out per GPU, > the 126 MB L2, so no flush is needed).
+Multi-GPU (torchrun): every rank runs the same per-GPU batch on its own device
+(weak scaling, independent launches, no collective on the data path); the
+device time is the max over ranks (one all_reduce of a scalar).
+
+* ``value``     -- GFLOP/s (5*N*log2N per transform), inputs resident in HBM,
+                   CUDA events around the K launches on the launch stream.
+* ``e2e``       -- the same metric through the public API with pinned HOST
+                   buffers: ``execute(plan, host_in, out=host_out)`` ->
+                   sfft_execute_host (H2D + kernels + D2H every step).
+* ``roofline``  -- the FFT kernel vs the measured HBM copy bandwidth.
+* ``cpu_baseline`` -- the reference algorithm (oracle/, the batched restatement
+                   of stagefft) on all host cores, bounded sample, rank 0.
+
+``--impl reference`` times only the reference CPU path (oracle port, all host
+cores) on the same config and prints the same line shape.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "GFLOP/s"
+
+CONFIGS = {
+    # name: (n, batch, precision, direction, description)
+    "c2": (1024, 65536, "single", "forward", "fp32 forward C2C FFT N=1024 batch=65536 (BASELINE configs[1])"),
+    "c4": (2048, 131072, "double", "forward", "fp64 forward C2C FFT N=2048 batch=131072 (BASELINE configs[3])"),
+    "c5": (512, 262144, "single", "forward", "fp32 forward C2C FFT N=512 batch=262144 per GPU (BASELINE configs[4])"),
+}
+
+
+def flops_per_row(n: int) -> float:
+    return 5.0 * n * math.log2(n)
+
+
+def row_bytes(n: int, precision: str) -> int:
+    return n * (8 if precision == "single" else 16)
+
+
+# --------------------------------------------------------------------- peaks
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(workload)
+        return None if rec is None else float(rec["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling via NVML, in a thread."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.samples = []  # (t, sm_mhz, reasons_mask)
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _reasons(self):
+        nv = self.nvml
+        for fn in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            if hasattr(nv, fn):
+                return int(getattr(nv, fn)(self.h))
+        return 0
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), self._reasons()))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+
+    def stop(self):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
+
+    def summary(self, t0: float, t1: float):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        note = "timed region"
+        if not inside:  # region shorter than the sampling period: nearest samples
+            inside = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:3]
+            note = "nearest to timed region"
+        mask = 0
+        for s in inside:
+            mask |= s[2]
+        reasons = [name for bit, name in self.REASONS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(inside), "window": note}
+
+
+# -------------------------------------------------------------- CPU baseline
+def _cpu_worker(args):
+    """Transform one resident chunk of rows ``reps`` times; returns (seconds, rows)."""
+    n, chunk_rows, reps, precision, direction, seed = args
+    import oracle
+
+    dtype = np.complex64 if precision == "single" else np.complex128
+    x = oracle.generate_batch(chunk_rows, n, seed, dtype)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.reference_execute(x, direction, dtype=dtype)
+    return time.perf_counter() - t0, chunk_rows * reps
+
+
+class CpuReference:
+    """The reference algorithm (oracle port) on all host cores.
+
+    One process per core (threads are useless under the GIL, BASELINE.md
+    section 2), each transforming its own chunk of Philox rows (<= 8 MiB, so
+    memory stays bounded); rate = total rows / slowest worker.
+    """
+
+    def __init__(self, n, precision, direction, procs=None):
+        import multiprocessing as mp
+
+        self.n, self.precision, self.direction = n, precision, direction
+        self.procs = procs or os.cpu_count() or 1
+        self.chunk = max(1, min((8 << 20) // row_bytes(n, precision), 1 << 16))
+        self.pool = mp.get_context("spawn").Pool(self.procs)
+        res = self._map(1)  # warm imports, calibrate
+        self.sec_per_rep = max(t for t, _ in res)
+
+    def _map(self, reps):
+        args = [(self.n, self.chunk, reps, self.precision, self.direction, i) for i in range(self.procs)]
+        return self.pool.map(_cpu_worker, args)
+
+    def rate(self, target_s):
+        reps = max(1, int(round(target_s / max(self.sec_per_rep, 1e-6))))
+        res = self._map(reps)
+        wall = max(t for t, _ in res)
+        total = sum(r for _, r in res)
+        sample = (f"{self.procs} processes x {reps} x {self.chunk} Philox rows "
+                  f"(N={self.n}, {self.precision}, {self.direction}) in {wall:.1f}s")
+        return total / wall, self.procs, sample
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_gpu(args, n, batch, precision, direction, workload):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_09384_b200 as sf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        return sf.sharding.max_over_ranks(v, device=dev)
+
+    cdt = torch.complex64 if precision == "single" else torch.complex128
+    ndt = np.complex64 if precision == "single" else np.complex128
+    rb = row_bytes(n, precision)
+    plan = sf.make_plan(n, direction, precision=precision)
+
+    # inputs: Philox rows (seeded per rank) in pinned host memory, then HBM
+    h_in = torch.empty((batch, n), dtype=cdt, pin_memory=True)
+    h_out = torch.empty((batch, n), dtype=cdt, pin_memory=True)
+    sf.generate_batch(batch, n, seed=rank, precision=precision, out=h_in.numpy())
+    x = h_in.to(dev)
+    y = torch.empty_like(x)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+
+    # ---- device-resident timed region: K launches, events on the launch stream
+    for _ in range(args.warmup):
+        sf.launch(plan, x, y, batch, stream=stream, flag=flag)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    region0 = torch.cuda.Event(enable_timing=True)
+    region1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    t_host0 = time.perf_counter()
+    region0.record(stream)
+    for k in range(args.steps):
+        evs[k][0].record(stream)
+        sf.launch(plan, x, y, batch, stream=stream, flag=flag)
+        evs[k][1].record(stream)
+    region1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_host1 = time.perf_counter()
+    barrier()
+    torch.cuda.synchronize(dev)
+    if int(flag.item()):
+        raise RuntimeError("non-finite flag raised on finite synthetic input")
+    region_ms = max_over_ranks(region0.elapsed_time(region1))
+    kernel_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in evs))
+    clock_info = clocks.summary(t_host0, t_host1)
+
+    # spot parity of the timed output (first rows) against the oracle, rank 0
+    parity = None
+    if rank == 0 and not args.no_check:
+        import oracle
+
+        rows = min(batch, 64)
+        want = oracle.reference_execute(h_in.numpy()[:rows], direction, dtype=ndt)
+        got = y[:rows].cpu().numpy()
+        parity = float(np.max(np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)))
+
+    # ---- e2e: public API on pinned host buffers (H2D + kernels + D2H)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    hin_np, hout_np = h_in.numpy(), h_out.numpy()
+    for _ in range(min(args.warmup, 2)):
+        sf.execute(plan, hin_np, out=hout_np)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sf.execute(plan, hin_np, out=hout_np)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    clocks.stop()
+    if rank == 0 and not args.no_check:
+        assert np.array_equal(hout_np[:64], y[:64].cpu().numpy()), "e2e output differs from device output"
+
+    total_rows = batch * world
+    fl = flops_per_row(n)
+    value = total_rows * fl / (region_ms / args.steps * 1e-3) / 1e9
+    e2e_value = total_rows * fl / e2e_s / 1e9
+    peak, peak_src = hbm_peak()
+    achieved = batch * 2 * rb / (kernel_ms * 1e-3) / 1e9
+    info = plan.kernel_info(local)
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(region_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32)" if precision == "single" else "c128 (fp64)",
+        "data": "synthetic Philox-uniform complex rows (signalgen random kind), seeded per rank",
+        "config": {
+            "workload": workload,
+            "n": n,
+            "batch_per_gpu": batch,
+            "global_batch": total_rows,
+            "precision": precision,
+            "direction": direction,
+            "parallelism": f"batch-sharded x{world} (independent launches, no collective)",
+            "l2_policy": f"input {batch * rb / 2**20:.0f} MiB per GPU > 126 MB L2; no flush needed",
+            "kernel": {k: info[k] for k in ("kernel", "elems_per_thread", "seqs_per_cta", "threads_per_cta", "radices", "variant")},
+        },
+        "e2e": {
+            "value": round(e2e_value, 1),
+            "unit": UNIT,
+            "h2d_bytes_per_step": batch * rb,
+            "d2h_bytes_per_step": batch * rb,
+            "path": "execute(plan, pinned numpy, out=pinned numpy) -> sfft_execute_host",
+            "ms_per_step": round(e2e_s * 1e3, 3),
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": ncu_traffic(workload),
+            "algorithmic_bytes_per_launch": batch * 2 * rb,
+            "kernel_ms": round(kernel_ms, 4),
+            "peak_source": peak_src,
+            "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
+        },
+        "gpu_launches": args.steps,
+        "clocks": clock_info,
+        "parity_rel_l2_max_first64": parity,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = CpuReference(n, precision, direction)
+        rate, cores, sample = cpu.rate(args.cpu_seconds)
+        cpu.close()
+        out["cpu_baseline"] = {"value": round(rate * fl / 1e9, 4), "unit": UNIT, "cores": cores,
+                               "kind": "port", "sample": sample,
+                               "rows_per_s": round(rate, 1)}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, n, batch, precision, direction, workload):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return  # rank 0 alone times the host CPU
+    fl = flops_per_row(n)
+    # each step is a bounded sample sized so warmup+steps ends in a few minutes
+    per_step = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    cpu = CpuReference(n, precision, direction)
+    for _ in range(args.warmup):
+        cpu.rate(per_step / 4)
+    rates = []
+    sample = ""
+    cores = 1
+    for _ in range(args.steps):
+        rate, cores, sample = cpu.rate(per_step)
+        rates.append(rate)
+    cpu.close()
+    rate = statistics.median(rates)
+    value = rate * fl / 1e9
+    out = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(batch / rate * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32)" if precision == "single" else "c128 (fp64)",
+        "data": "synthetic Philox-uniform complex rows",
+        "config": {"workload": workload, "n": n, "batch_per_gpu": batch, "precision": precision,
+                   "direction": direction, "parallelism": "host CPU, one process per core"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference = stagefft algorithm restated batched in numpy (oracle/stagefft_port.py); "
+                "ms_per_step extrapolates the sampled rate to the full batch",
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--n", type=int)
+    ap.add_argument("--batch", type=int)
+    ap.add_argument("--precision", choices=["single", "double"])
+    ap.add_argument("--direction", choices=["forward", "inverse"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    n, batch, precision, direction, workload = CONFIGS[args.config]
+    if any(v is not None for v in (args.n, args.batch, args.precision, args.direction)):
+        n = args.n or n
+        precision = args.precision or precision
+        batch = args.batch or (1 << 30) // row_bytes(n, precision)
+        direction = args.direction or direction
+        workload = f"{'fp32' if precision == 'single' else 'fp64'} {direction} C2C FFT N={n} batch={batch}"
+    if args.impl == "reference":
+        run_reference(args, n, batch, precision, direction, workload)
+    else:
+        run_gpu(args, n, batch, precision, direction, workload)
+
+
+if __name__ == "__main__":
+    main()

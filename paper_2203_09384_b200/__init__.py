@@ -35,7 +35,8 @@ from .planner import (
     factorize_stages,
     make_plan,
 )
-from .sharding import execute_sharded, shard_bounds
+from . import sharding
+from .sharding import execute_sharded, max_over_ranks, shard_bounds
 from .signalgen import KINDS, generate, generate_batch
 
 try:
@@ -79,6 +80,7 @@ __all__ = [
     "is_power_of_two",
     "launch",
     "make_plan",
+    "max_over_ranks",
     "shard_bounds",
     "twiddle",
 ]

@@ -142,8 +142,10 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {stockham_variant<float, 128, 8, 8>(), stockham_variant<float, 128, 16, 16>()},
           {stockham_variant<float, 256, 16, 8>(), stockham_variant<float, 256, 8, 4>()},
           {stockham_variant<float, 512, 16, 4>(), stockham_variant<float, 512, 8, 2>()},
-          {stockham_variant<float, 1024, 16, 2>(), stockham_variant<float, 1024, 8, 1>()},
-          {stockham_variant<float, 2048, 16, 1>(), stockham_variant<float, 2048, 8, 1>()},
+          {stockham_variant<float, 1024, 16, 1>(), stockham_variant<float, 1024, 8, 1>(),
+           stockham_variant<float, 1024, 16, 2>(), stockham_variant<float, 1024, 32, 4>()},
+          {stockham_variant<float, 2048, 16, 1>(), stockham_variant<float, 2048, 8, 1>(),
+           stockham_variant<float, 2048, 32, 2>()},
       },
       {
           {},
@@ -156,7 +158,8 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {stockham_variant<double, 128, 8, 8>(), stockham_variant<double, 128, 16, 16>()},
           {stockham_variant<double, 256, 8, 4>(), stockham_variant<double, 256, 16, 8>()},
           {stockham_variant<double, 512, 8, 2>(), stockham_variant<double, 512, 16, 4>()},
-          {stockham_variant<double, 1024, 8, 1>(), stockham_variant<double, 1024, 16, 2>()},
+          {stockham_variant<double, 1024, 8, 1>(), stockham_variant<double, 1024, 16, 2>(),
+           stockham_variant<double, 1024, 16, 1>()},
           {stockham_variant<double, 2048, 16, 1>(), stockham_variant<double, 2048, 8, 1>()},
       },
   };

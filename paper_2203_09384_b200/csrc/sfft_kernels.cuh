@@ -77,13 +77,28 @@ __device__ __forceinline__ int swz_elem(int e) {
 // 16-byte-chunk swizzle for the tile kernel (8 chunks per bank row).
 __device__ __forceinline__ int swz_chunk(int c) { return c ^ (((c >> 3) ^ (c >> 6)) & 7); }
 
-template <int G>
+template <int ID, int COUNT>
+__device__ __forceinline__ void named_bar() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
+}
+
+// Barrier over the G threads of one sequence.  Barrier ids are compile-time
+// immediates so ptxas reserves only the ids actually used (a register id
+// makes it reserve all 16 per CTA).
+template <int G, int SEQ>
 __device__ __forceinline__ void seq_sync(int s) {
   if constexpr (G <= 32) {
     __syncwarp();
+  } else if constexpr (SEQ == 1) {
+    __syncthreads();
   } else {
-    // named barrier per sequence: only the G threads of one sequence wait
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(G) : "memory");
+    static_assert(SEQ <= 4, "named barrier ids 1..4");
+    switch (s) {  // warp-uniform
+      case 0: named_bar<1, G>(); break;
+      case 1: named_bar<2, G>(); break;
+      case 2: named_bar<3, G>(); break;
+      default: named_bar<4, G>(); break;
+    }
   }
 }
 
@@ -96,7 +111,7 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
   constexpr int G = N / R;
   constexpr int NP = num_passes(N, R);
   static_assert(G >= 1 && (N % R) == 0, "geometry");
-  static_assert(G <= 32 || SEQ <= 15, "named barrier ids");
+  static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* sm = reinterpret_cast<C*>(smem_raw);
@@ -172,7 +187,7 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
         }
       }
     } else {
-      if constexpr (p > 0) seq_sync<G>(s);  // everyone has read before we overwrite
+      if constexpr (p > 0) seq_sync<G, SEQ>(s);  // everyone has read before we overwrite
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int b = j + t * G;
@@ -181,7 +196,7 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
 #pragma unroll
         for (int q = 0; q < r; ++q) sm[swz_elem<T>(sbase + base + q * L)] = v[t + q * NB];
       }
-      seq_sync<G>(s);
+      seq_sync<G, SEQ>(s);
     }
   });
 }

@@ -81,9 +81,18 @@ def _prepare_host(plan: FftPlan, signal):
     return x, xc, rows
 
 
-def _execute_host(plan: FftPlan, signal):
+def _execute_host(plan: FftPlan, signal, out=None):
     x, xc, rows = _prepare_host(plan, signal)
-    out = np.empty(xc.shape, dtype=plan.dtype)
+    if out is None:
+        out = np.empty(xc.shape, dtype=plan.dtype)
+    elif (
+        not isinstance(out, np.ndarray)
+        or out.dtype != plan.dtype
+        or out.size != xc.size
+        or not out.flags.c_contiguous
+        or out.ctypes.data % 16
+    ):
+        raise ShapeError("out must be a C-contiguous, 16-byte aligned array of the plan dtype and size")
     handle = plan.native_handle(_default_device(plan))
     _native.check(_native.lib().sfft_execute_host(handle, xc.ctypes.data, out.ctypes.data, rows))
     return out
@@ -124,10 +133,20 @@ def launch(plan: FftPlan, x_in, x_out, rows: int, *, stream=None, flag=None) -> 
     )
 
 
-def _execute_device(plan: FftPlan, x, timed: bool = False):
+def _execute_device(plan: FftPlan, x, timed: bool = False, out=None):
     t0 = time.perf_counter_ns()
     xc, rows = _prepare_device(plan, x)
-    out = torch.empty_like(xc)
+    if out is None:
+        out = torch.empty_like(xc)
+    elif (
+        not _is_torch(out)
+        or out.device != xc.device
+        or out.dtype != xc.dtype
+        or out.numel() != xc.numel()
+        or not out.is_contiguous()
+        or out.data_ptr() % 16
+    ):
+        raise ShapeError("out must be a contiguous, 16-byte aligned tensor of the plan dtype on the input device")
     flag = torch.zeros(1, dtype=torch.int32, device=xc.device)
     stream = torch.cuda.current_stream(xc.device)
     if timed:
@@ -145,13 +164,18 @@ def _execute_device(plan: FftPlan, x, timed: bool = False):
 
 
 # ----------------------------------------------------------------- public API
-def execute(plan: FftPlan, signal):
-    """Run ``plan`` on ``signal`` and return fresh output (executor.py:50-52)."""
+def execute(plan: FftPlan, signal, *, out=None):
+    """Run ``plan`` on ``signal`` and return fresh output (executor.py:50-52).
+
+    ``out`` (optional, not in the reference) receives the result instead of a
+    fresh allocation -- e.g. a pinned host array, so the D2H copy runs at full
+    DMA rate.  It must not alias ``signal`` unless in-place is intended.
+    """
     if _is_torch(signal):
         if signal.is_cuda:
-            return _execute_device(plan, signal)[0]
-        return torch.from_numpy(_execute_host(plan, signal.numpy()))
-    return _execute_host(plan, signal)
+            return _execute_device(plan, signal, out=out)[0]
+        return torch.from_numpy(_execute_host(plan, signal.numpy(), None if out is None else out.numpy()))
+    return _execute_host(plan, signal, out)
 
 
 def execute_timed(plan: FftPlan, signal) -> TimedExecution:

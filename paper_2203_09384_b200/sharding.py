@@ -34,6 +34,24 @@ def shard_bounds(batch: int, world: int, rank: int) -> tuple[int, int]:
     return start, min(batch, start + per)
 
 
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank scalar (device time) over the process group.
+
+    Multi-GPU numbers are timed on each device and reduced with MAX, never
+    by wall clock; with no process group this is the identity.
+    """
+    try:
+        import torch
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return float(value)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def execute_sharded(plan: FftPlan, signal, devices) -> np.ndarray:
     """Run a (B, N) host batch split across ``devices``; returns numpy (B, N)."""
     devices = [int(d) for d in devices]
