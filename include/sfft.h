@@ -70,6 +70,8 @@ typedef struct sfft_plan_info {
   int32_t radices[8];          /* GPU pass radices, first to last */
   int64_t twiddle_elems;       /* per-pass twiddle table length (elements) */
   int32_t variant;             /* index into the kernel variant table */
+  int32_t layout;              /* stockham smem layout: 0 xor swizzle, 1 padded */
+  int32_t twiddle_policy;      /* 0: every twiddle loaded; 1: powers of two + products */
   int32_t reserved;
 } sfft_plan_info_t;
 

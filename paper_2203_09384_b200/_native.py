@@ -56,6 +56,8 @@ class PlanInfo(ctypes.Structure):
         ("radices", ctypes.c_int32 * 8),
         ("twiddle_elems", ctypes.c_int64),
         ("variant", ctypes.c_int32),
+        ("layout", ctypes.c_int32),
+        ("twiddle_policy", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
     ]
 

@@ -36,6 +36,8 @@ struct Variant {
   int kernel;      // SFFT_KERNEL_*
   int r;           // elements per thread (stockham R; tile: n)
   int seq;         // sequences per CTA
+  int layout;      // smem layout (stockham): 0 xor swizzle, 1 padded
+  int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products
   int threads;     // threads per CTA
   int smem;        // dynamic smem bytes
   int passes;
@@ -46,23 +48,28 @@ struct Variant {
 };
 
 // ---------------------------------------------------------------- launchers
-template <typename T, int N, int R, int SEQ, bool INV>
+template <typename T, int N, int R, int SEQ, int LAYOUT>
+constexpr int stockham_smem() {
+  return SEQ * sfft::Smem<T, LAYOUT, R>::size(N) * int(sizeof(sfft::cx_t<T>));
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
 cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
                             cudaStream_t st) {
   using C = sfft::cx_t<T>;
   constexpr int threads = (N / R) * SEQ;
-  constexpr int smem = SEQ * N * int(sizeof(C));
+  constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   const long long grid = (batch + SEQ - 1) / SEQ;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  sfft::stockham_kernel<T, N, R, SEQ, INV><<<dim3(unsigned(grid)), threads, smem, st>>>(
+  sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP><<<dim3(unsigned(grid)), threads, smem, st>>>(
       static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
   return cudaGetLastError();
 }
-template <typename T, int N, int R, int SEQ, bool INV>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
 cudaError_t prepare_stockham() {
-  constexpr int smem = SEQ * N * int(sizeof(sfft::cx_t<T>));
-  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              stockham_smem<T, N, R, SEQ, LAYOUT>());
 }
 
 template <typename T>
@@ -89,21 +96,23 @@ cudaError_t prepare_tile() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-template <typename T, int N, int R, int SEQ>
+template <typename T, int N, int R, int SEQ, int LAYOUT = 0, int TWP = 0>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
   v.r = R;
   v.seq = SEQ;
+  v.layout = LAYOUT;
   v.threads = (N / R) * SEQ;
-  v.smem = SEQ * N * int(sizeof(sfft::cx_t<T>));
+  v.smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   v.passes = sfft::num_passes(N, R);
   for (int p = 0; p < v.passes && p < 8; ++p) v.radices[p] = sfft::pass_radix(N, R, p);
   v.tw_len = sfft::twiddle_table_len(N, R);
-  v.launch[0] = &launch_stockham<T, N, R, SEQ, false>;
-  v.launch[1] = &launch_stockham<T, N, R, SEQ, true>;
-  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false>;
-  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true>;
+  v.twp = TWP;
+  v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP>;
+  v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP>;
+  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP>;
+  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP>;
   return v;
 }
 
@@ -137,30 +146,36 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<float, 4, 4, 4>(), tile_variant<float, 4, 2, 8>()},
           {tile_variant<float, 8, 4, 4>(), tile_variant<float, 8, 2, 4>()},
           {tile_variant<float, 16, 2, 4>(), tile_variant<float, 16, 1, 8>()},
-          {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32>()},
-          {stockham_variant<float, 64, 8, 16>(), stockham_variant<float, 64, 16, 32>()},
-          {stockham_variant<float, 128, 8, 8>(), stockham_variant<float, 128, 16, 16>()},
-          {stockham_variant<float, 256, 16, 8>(), stockham_variant<float, 256, 8, 4>()},
-          {stockham_variant<float, 512, 16, 4>(), stockham_variant<float, 512, 8, 2>()},
-          {stockham_variant<float, 1024, 16, 1>(), stockham_variant<float, 1024, 8, 1>(),
-           stockham_variant<float, 1024, 16, 2>(), stockham_variant<float, 1024, 32, 4>()},
-          {stockham_variant<float, 2048, 16, 1>(), stockham_variant<float, 2048, 8, 1>(),
-           stockham_variant<float, 2048, 32, 2>()},
+          {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32, 1>()},
+          {stockham_variant<float, 64, 8, 16, 1>(), stockham_variant<float, 64, 16, 32, 1>()},
+          {stockham_variant<float, 128, 16, 16, 0>(), stockham_variant<float, 128, 16, 16, 1>(),
+           stockham_variant<float, 128, 8, 8, 1>()},
+          {stockham_variant<float, 256, 16, 8, 1>(), stockham_variant<float, 256, 16, 8, 0>(),
+           stockham_variant<float, 256, 16, 8, 1, 1>()},
+          {stockham_variant<float, 512, 16, 4, 1, 1>(), stockham_variant<float, 512, 16, 2, 1>(),
+           stockham_variant<float, 512, 16, 4, 1>()},
+          {stockham_variant<float, 1024, 16, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1>(),
+           stockham_variant<float, 1024, 32, 4, 1>(), stockham_variant<float, 1024, 16, 2, 1>()},
+          {stockham_variant<float, 2048, 16, 1, 1, 1>(), stockham_variant<float, 2048, 16, 1, 1>(),
+           stockham_variant<float, 2048, 16, 1, 0>(), stockham_variant<float, 2048, 32, 1, 1>()},
       },
       {
           {},
           {tile_variant<double, 2, 4, 4>(), tile_variant<double, 2, 2, 8>()},
           {tile_variant<double, 4, 2, 4>(), tile_variant<double, 4, 1, 8>()},
           {tile_variant<double, 8, 1, 4>(), tile_variant<double, 8, 2, 4>()},
-          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64>()},
-          {stockham_variant<double, 32, 8, 32>(), stockham_variant<double, 32, 16, 64>()},
-          {stockham_variant<double, 64, 8, 16>(), stockham_variant<double, 64, 16, 32>()},
-          {stockham_variant<double, 128, 8, 8>(), stockham_variant<double, 128, 16, 16>()},
-          {stockham_variant<double, 256, 8, 4>(), stockham_variant<double, 256, 16, 8>()},
-          {stockham_variant<double, 512, 8, 2>(), stockham_variant<double, 512, 16, 4>()},
-          {stockham_variant<double, 1024, 8, 1>(), stockham_variant<double, 1024, 16, 2>(),
-           stockham_variant<double, 1024, 16, 1>()},
-          {stockham_variant<double, 2048, 16, 1>(), stockham_variant<double, 2048, 8, 1>()},
+          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64, 0>()},
+          {stockham_variant<double, 32, 8, 32, 1>(), stockham_variant<double, 32, 8, 32, 0>()},
+          {stockham_variant<double, 64, 8, 16, 1>(), stockham_variant<double, 64, 8, 16, 0>()},
+          {stockham_variant<double, 128, 16, 16, 0>(), stockham_variant<double, 128, 8, 8, 1>()},
+          {stockham_variant<double, 256, 16, 8, 0, 1>(), stockham_variant<double, 256, 8, 4, 1>(),
+           stockham_variant<double, 256, 16, 8, 0>()},
+          {stockham_variant<double, 512, 16, 4, 0, 1>(), stockham_variant<double, 512, 16, 2, 0>(),
+           stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 0>()},
+          {stockham_variant<double, 1024, 16, 2, 0, 1>(), stockham_variant<double, 1024, 16, 1, 0, 1>(),
+           stockham_variant<double, 1024, 16, 1, 0>(), stockham_variant<double, 1024, 8, 1, 0>()},
+          {stockham_variant<double, 2048, 16, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 0>(),
+           stockham_variant<double, 2048, 8, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 1>()},
       },
   };
   return table[precision][log2n];
@@ -396,6 +411,8 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   for (int i = 0; i < 8; ++i) info->radices[i] = p->v->radices[i];
   info->twiddle_elems = p->v->tw_len;
   info->variant = p->variant;
+  info->layout = p->v->layout;
+  info->twiddle_policy = p->v->twp;
   return SFFT_OK;
 }
 
@@ -420,6 +437,8 @@ int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_i
   for (int i = 0; i < 8; ++i) info->radices[i] = v.radices[i];
   info->twiddle_elems = v.tw_len;
   info->variant = variant;
+  info->layout = v.layout;
+  info->twiddle_policy = v.twp;
   return SFFT_OK;
 }
 

@@ -65,12 +65,53 @@ __host__ __device__ constexpr double cos32(int j) {
 __host__ __device__ constexpr double sin32(int j) { return cos32(8 - j + 32); }
 
 // ------------------------------------------------------------ complex helpers
+// fp64: scalar DADD/DFMA.  fp32: Blackwell's packed FP32x2 pipe (FADD2 /
+// FMUL2 / FFMA2): one instruction updates re and im together.  Swaps and
+// single-lane negations written as make_float2(b.y, -b.x) cost nothing --
+// ptxas folds them into the .F32x2.LO_HI / .NP operand modifiers -- so +-i
+// rotations stay free and a complex multiply is 2 instructions.
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return C{a.x + b.x, a.y + b.y}; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { return C{a.x - b.x, a.y - b.y}; }
 template <typename C> __device__ __forceinline__ C cmul(C a, C w) {
   return C{a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
 }
+
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) {
+  return (static_cast<unsigned long long>(__float_as_uint(a.y)) << 32) | __float_as_uint(a.x);
+}
+__device__ __forceinline__ float2 f2_from(unsigned long long r) {
+  return make_float2(__uint_as_float(static_cast<uint32_t>(r)), __uint_as_float(static_cast<uint32_t>(r >> 32)));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(r);
+}
+template <> __device__ __forceinline__ float2 cadd<float2>(float2 a, float2 b) { return add2(a, b); }
+template <> __device__ __forceinline__ float2 csub<float2>(float2 a, float2 b) { return sub2(a, b); }
+// a*w = a.x*(w.x, w.y) + a.y*(-w.y, w.x)
+template <> __device__ __forceinline__ float2 cmul<float2>(float2 a, float2 w) {
+  return fma2(make_float2(a.y, a.y), make_float2(-w.y, w.x), mul2(make_float2(a.x, a.x), w));
+}
+
 template <typename C> __device__ __forceinline__ C cswap(C a) { return C{a.y, a.x}; }
+template <typename C> __device__ __forceinline__ C mul_minus_i(C a) { return C{a.y, -a.x}; }
+template <typename C> __device__ __forceinline__ C mul_plus_i(C a) { return C{-a.y, a.x}; }
 
 // a * exp(-2*pi*i*J/L) with J, L compile-time, L a power of two <= 32.
 template <int J, int L, typename C>
@@ -82,23 +123,41 @@ __device__ __forceinline__ C twiddle_const(C a) {
     return a;
   } else if constexpr (2 * j == L) {
     return C{-a.x, -a.y};
-  } else if constexpr (4 * j == L) {  // -i
-    return C{a.y, -a.x};
-  } else if constexpr (4 * j == 3 * L) {  // +i
-    return C{-a.y, a.x};
-  } else if constexpr (8 * j == L) {  // (1 - i)/sqrt2
-    return C{(a.x + a.y) * h, (a.y - a.x) * h};
-  } else if constexpr (8 * j == 3 * L) {  // (-1 - i)/sqrt2
-    return C{(a.y - a.x) * h, -(a.x + a.y) * h};
-  } else if constexpr (8 * j == 5 * L) {  // (-1 + i)/sqrt2
-    return C{-(a.x + a.y) * h, (a.x - a.y) * h};
-  } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
-    return C{(a.x - a.y) * h, (a.x + a.y) * h};
+  } else if constexpr (4 * j == L) {
+    return mul_minus_i(a);
+  } else if constexpr (4 * j == 3 * L) {
+    return mul_plus_i(a);
+  } else if constexpr (std::is_same_v<C, float2>) {
+    // eighth roots: h*(a + rot*a) with rot in {-i, +i}; others: 2-op cmul
+    if constexpr (8 * j == L) {  // (1 - i)/sqrt2
+      return mul2(add2(a, mul_minus_i(a)), make_float2(h, h));
+    } else if constexpr (8 * j == 3 * L) {  // (-1 - i)/sqrt2 = -i * (1 - i)/sqrt2 ... = h*(-a - i a)
+      return mul2(add2(mul_minus_i(a), C{-a.x, -a.y}), make_float2(h, h));
+    } else if constexpr (8 * j == 5 * L) {  // (-1 + i)/sqrt2
+      return mul2(add2(mul_plus_i(a), C{-a.x, -a.y}), make_float2(h, h));
+    } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
+      return mul2(add2(a, mul_plus_i(a)), make_float2(h, h));
+    } else {
+      constexpr int j32 = j * (32 / L);
+      constexpr T c = T(cos32(j32));
+      constexpr T s = T(-sin32(j32));
+      return fma2(make_float2(a.y, a.y), make_float2(-s, c), mul2(make_float2(a.x, a.x), make_float2(c, s)));
+    }
   } else {
-    constexpr int j32 = j * (32 / L);
-    constexpr T c = T(cos32(j32));
-    constexpr T s = T(-sin32(j32));
-    return cmul(a, C{c, s});
+    if constexpr (8 * j == L) {  // (1 - i)/sqrt2
+      return C{(a.x + a.y) * h, (a.y - a.x) * h};
+    } else if constexpr (8 * j == 3 * L) {  // (-1 - i)/sqrt2
+      return C{(a.y - a.x) * h, -(a.x + a.y) * h};
+    } else if constexpr (8 * j == 5 * L) {  // (-1 + i)/sqrt2
+      return C{-(a.x + a.y) * h, (a.x - a.y) * h};
+    } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
+      return C{(a.x - a.y) * h, (a.x + a.y) * h};
+    } else {
+      constexpr int j32 = j * (32 / L);
+      constexpr T c = T(cos32(j32));
+      constexpr T s = T(-sin32(j32));
+      return cmul(a, C{c, s});
+    }
   }
 }
 
@@ -154,5 +213,6 @@ __device__ __forceinline__ uint32_t nonfinite_bits(double2 v) {
 
 template <typename C, typename T>
 __device__ __forceinline__ C cscale(C a, T s) { return C{a.x * s, a.y * s}; }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return mul2(a, make_float2(s, s)); }
 
 }  // namespace sfft

@@ -30,8 +30,10 @@
 namespace sfft {
 
 // ------------------------------------------------------------ pass schedule
-// N = r0 * R^(P-1) with the (smaller) remainder radix r0 first: pass 0 has
-// stride 1 and therefore needs no twiddles at all.
+// N = R^(P-1) * r_last with the (smaller) remainder radix LAST: pass 0 has
+// stride 1 (no twiddles) and every exchange written before the last pass has
+// stride L >= R, which keeps the swizzled scatters conflict-free per
+// quarter/half-warp phase (tests/test_bank_model.py).
 __host__ __device__ constexpr int remainder_radix(int n, int r) {
   while (n % r == 0 && n > 1) n /= r;
   return n;
@@ -43,7 +45,7 @@ __host__ __device__ constexpr int num_passes(int n, int r) {
   return p + (m > 1 ? 1 : 0);
 }
 __host__ __device__ constexpr int pass_radix(int n, int r, int p) {
-  return (remainder_radix(n, r) > 1 && p == 0) ? remainder_radix(n, r) : r;
+  return (remainder_radix(n, r) > 1 && p == num_passes(n, r) - 1) ? remainder_radix(n, r) : r;
 }
 __host__ __device__ constexpr int pass_stride(int n, int r, int p) {
   int l = 1;
@@ -61,19 +63,39 @@ __host__ __device__ constexpr int twiddle_table_len(int n, int r) {
   return pass_twiddle_offset(n, r, num_passes(n, r));
 }
 
-// --------------------------------------------------------- smem swizzles
-// Element-granular XOR swizzle: 128-byte bank rows hold 16 fp32 complex or
-// 8 fp64 complex; two XOR terms make every Stockham read and write pattern
-// of the configured (N, R) pairs conflict-free (tests/test_bank_model.py
-// checks this with a bank model).
-template <typename T>
-__device__ __forceinline__ int swz_elem(int e) {
-  if constexpr (sizeof(T) == 4) {
-    return e ^ (((e >> 4) ^ (e >> 8)) & 15);
-  } else {
-    return e ^ (((e >> 3) ^ (e >> 6)) & 7);
+// ------------------------------------------------------- smem layouts
+// Bank rows are 128 bytes = 16 fp32 / 8 fp64 complex; a warp access is served
+// per phase of 16 (8-byte) or 8 (16-byte) lanes.
+// LAYOUT 0: element XOR swizzle over the CTA-wide index.
+// LAYOUT 1: per-sequence region with one pad element after every R elements.
+//           Stride-R scatters become stride R+1 (odd), and addresses factor:
+//           map(base + c) = map(base) + c + c/R for c a multiple of R, so a
+//           pass's gathers are one base register plus immediate offsets.
+// tests/test_bank_model.py replays every access of every variant per phase.
+template <typename T, int LAYOUT, int R>
+struct Smem {
+  __host__ __device__ static constexpr int size(int n) { return LAYOUT == 1 ? n + n / R : n; }
+  __device__ static __forceinline__ int map(int e) {
+    if constexpr (LAYOUT == 1) {
+      return e + e / R;
+    } else if constexpr (sizeof(T) == 4) {
+      return e ^ (((e >> 4) ^ (e >> 8)) & 15);
+    } else {
+      return e ^ (((e >> 3) ^ (e >> 6)) & 7);
+    }
   }
-}
+  // map(base + off), off folds to a constant after unrolling; `base_aligned`
+  // promises base % R == 0 (so off < R stays inside one padded row).
+  __device__ static __forceinline__ int map2(int base, int mapped_base, int off,
+                                             bool base_aligned = false) {
+    if constexpr (LAYOUT == 1) {
+      if (off % R == 0) return mapped_base + off + off / R;
+      if (base_aligned && off < R) return mapped_base + off;
+    }
+    return map(base + off);
+  }
+};
+
 // 16-byte-chunk swizzle for the tile kernel (8 chunks per bank row).
 __device__ __forceinline__ int swz_chunk(int c) { return c ^ (((c >> 3) ^ (c >> 6)) & 7); }
 
@@ -103,13 +125,54 @@ __device__ __forceinline__ void seq_sync(int s) {
 }
 
 // ---------------------------------------------------------- Stockham kernel
-template <typename T, int N, int R, int SEQ, bool INV>
+template <typename T>
+__device__ __forceinline__ void accumulate_nonfinite(float2& acc, uint32_t&, float2 v) {
+  acc = fma2(v, make_float2(0.f, 0.f), acc);  // Inf/NaN * 0 = NaN, sticky
+}
+template <typename T>
+__device__ __forceinline__ void accumulate_nonfinite(float2&, uint32_t& bad, double2 v) {
+  bad |= nonfinite_bits(v);
+}
+
+__host__ __device__ constexpr int high_pow2(int q) {
+  int h = 1;
+  while (h * 2 <= q) h *= 2;
+  return h;
+}
+
+// Apply the pass twiddles w^q, w = w_{L r}^k, to one butterfly's operands.
+// TWP 0: every w^q is its own table entry (r-1 loads, exact table values).
+// TWP 1: only w^(2^i) are loaded; w^q = w^hi * w^(q-hi) (<= 3 products deep,
+//        error <= ~3 ulp) -- trades L1 wavefronts for FMA-pipe work.
+template <int TWP, int r, int L, int NB, typename C, int R>
+__device__ __forceinline__ void apply_pass_twiddles(C (&v)[R], const C* __restrict__ tp, int t) {
+  if constexpr (TWP == 0) {
+#pragma unroll
+    for (int q = 1; q < r; ++q) v[t + q * NB] = cmul(v[t + q * NB], __ldg(tp + (q - 1) * L));
+  } else {
+    C w[r];
+    static_for<1, r>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      if constexpr ((q & (q - 1)) == 0) {
+        w[q] = __ldg(tp + (q - 1) * L);
+      } else {
+        constexpr int hi = high_pow2(q);
+        w[q] = cmul(w[hi], w[q - hi]);
+      }
+      v[t + q * NB] = cmul(v[t + q * NB], w[q]);
+    });
+  }
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
 __global__ void __launch_bounds__((N / R) * SEQ)
 stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
                 const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
   using C = cx_t<T>;
+  using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
   constexpr int NP = num_passes(N, R);
+  constexpr int SN = S::size(N);  // smem elements per sequence
   static_assert(G >= 1 && (N % R) == 0, "geometry");
   static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
 
@@ -121,7 +184,10 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
   const int j = tid - s * G;
   const long long seq = (long long)blockIdx.x * SEQ + s;
   const bool valid = seq < batch;
-  const int sbase = s * N;
+  // LAYOUT 1 keeps each sequence in its own padded region; LAYOUT 0 swizzles
+  // the CTA-wide element index (sequences are N apart, N a multiple of 16).
+  const int sbase = LAYOUT == 1 ? 0 : s * N;
+  C* smq = LAYOUT == 1 ? sm + s * SN : sm;
 
   C v[R];
   if (valid) {
@@ -133,15 +199,18 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
     for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
   }
   if (nonfinite != nullptr) {
+    float2 acc = make_float2(0.f, 0.f);
     uint32_t bad = 0;
 #pragma unroll
-    for (int m = 0; m < R; ++m) bad |= nonfinite_bits(v[m]);
-    if (bad) atomicOr(nonfinite, 1);
+    for (int m = 0; m < R; ++m) accumulate_nonfinite<T>(acc, bad, v[m]);
+    if (bad || acc.x != acc.x || acc.y != acc.y) atomicOr(nonfinite, 1);
   }
   if constexpr (INV) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
   }
+  const int rbase = sbase + j;
+  const int rbase_m = S::map(rbase);
 
   static_for<0, NP>([&](auto P) {
     constexpr int p = decltype(P)::value;
@@ -151,17 +220,14 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
     if constexpr (p > 0) {
       // gather this pass's inputs x[j + m*G] from the exchange buffer
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = sm[swz_elem<T>(sbase + j + m * G)];
+      for (int m = 0; m < R; ++m) v[m] = smq[S::map2(rbase, rbase_m, m * G)];
       // twiddles w_{L r}^{q k}, k = b mod L  (kernels.py:41-72, gathered
       // from the plan table instead of rebuilt per call)
       const C* twp = tw + pass_twiddle_offset(N, R, p);
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int k = (j + t * G) & (L - 1);
-#pragma unroll
-        for (int q = 1; q < r; ++q) {
-          v[t + q * NB] = cmul(v[t + q * NB], __ldg(twp + (q - 1) * L + k));
-        }
+        apply_pass_twiddles<TWP, r, L, NB>(v, twp + k, t);
       }
     }
     // radix-r DFTs in registers
@@ -192,9 +258,11 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
       for (int t = 0; t < NB; ++t) {
         const int b = j + t * G;
         const int k = b & (L - 1);
-        const int base = (b - k) * r + k;
+        const int wbase = sbase + (b - k) * r + k;
+        const int wbase_m = S::map(wbase);
+        constexpr bool aligned = (L == 1 && r == R);  // wbase = b*R
 #pragma unroll
-        for (int q = 0; q < r; ++q) sm[swz_elem<T>(sbase + base + q * L)] = v[t + q * NB];
+        for (int q = 0; q < r; ++q) smq[S::map2(wbase, wbase_m, q * L, aligned)] = v[t + q * NB];
       }
       seq_sync<G, SEQ>(s);
     }

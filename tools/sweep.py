@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--n", default=",".join(str(2**p) for p in range(1, 12)))
     ap.add_argument("--dir", default="forward")
     ap.add_argument("--all-variants", action="store_true")
+    ap.add_argument("--variant", type=int, default=None)
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     peak = 6549.8
@@ -54,7 +55,8 @@ def main():
             x.imag.uniform_(-1, 1)
             y = torch.empty_like(x)
             nvar = lib.sfft_num_variants(n, 0 if prec == "single" else 1)
-            for v in range(nvar if args.all_variants else 1):
+            vlist = range(nvar) if args.all_variants else [args.variant or 0]
+            for v in vlist:
                 plan = sf.make_plan(n, args.dir, precision=prec, variant=v)
                 us = time_plan(plan, x, y, rows, args.iters, args.warmup)
                 gbs = 2 * rows * n * esz / us / 1e3
