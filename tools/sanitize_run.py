@@ -1,0 +1,36 @@
+"""Small launches of every compiled kernel variant, for compute-sanitizer.
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_run.py
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py --quick
+    compute-sanitizer --tool synccheck python tools/sanitize_run.py --quick
+
+Batches are odd-sized so partial CTAs / partial warp tiles are exercised.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2203_09384_b200 as sf  # noqa: E402
+
+quick = "--quick" in sys.argv
+lib = sf._native.lib()
+count = 0
+for prec in ("single", "double"):
+    for p in range(1, 12):
+        n = 2**p
+        nvar = lib.sfft_num_variants(n, 0 if prec == "single" else 1)
+        for v in range(1 if quick else nvar):
+            for d in ("forward", "inverse"):
+                batch = 37 if quick else 261
+                x = torch.from_numpy(sf.generate_batch(batch, n, seed=1, precision=prec)).cuda()
+                plan = sf.make_plan(n, d, precision=prec, variant=v)
+                y = sf.execute(plan, x)
+                buf = x.clone()
+                sf.launch(plan, buf, buf, batch)  # in-place
+                torch.cuda.synchronize()
+                assert torch.equal(buf, y)
+                count += 1
+print(f"sanitize_run: {count} launches OK")
