@@ -21,6 +21,7 @@ from .errors import (
     UnsupportedLengthError,
 )
 from .executor import TimedExecution, execute, execute_timed, launch
+from .kernels import count_butterflies, split_radix_transform
 from .numerics import TABLE_MAX_LENGTH, TwiddleTable, build_twiddle_table, is_power_of_two, twiddle
 from .planner import (
     ENGINE_MAX_LENGTH,
@@ -70,6 +71,7 @@ __all__ = [
     "TwiddleTable",
     "UnsupportedLengthError",
     "build_twiddle_table",
+    "count_butterflies",
     "digit_reversal_permutation",
     "execute",
     "execute_sharded",
@@ -82,5 +84,6 @@ __all__ = [
     "make_plan",
     "max_over_ranks",
     "shard_bounds",
+    "split_radix_transform",
     "twiddle",
 ]

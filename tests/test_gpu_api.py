@@ -1,0 +1,144 @@
+"""Reference-facing API on the GPU: estimator, execute_timed, acceptance criteria, sharding."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2203_09384_b200 as sf
+from conftest import rel_l2, row_rel_l2
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ENGINE_N = [2**p for p in range(3, 12)]
+
+
+def signals(rows, width, seed=0):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-1, 1, (rows, width)) + 1j * rng.uniform(-1, 1, (rows, width))).astype(np.complex64)
+
+
+def test_fit_transform_is_one_launch_and_bit_equal_to_execute(cuda):
+    X = signals(5, 64)
+    out = sf.FourierTransformer().fit_transform(X)
+    plan = sf.make_plan(64)
+    for row_in, row_out in zip(X, out):
+        assert np.array_equal(row_out, sf.execute(plan, row_in))  # test_estimator.py:16-23
+
+
+def test_estimator_golden_fixture(cuda, golden):
+    g = golden("estimator_c64.npz")
+    est = sf.FourierTransformer().fit(g["X"])
+    Y = est.transform(g["X"])
+    assert rel_l2(Y, g["Y"]) <= 1e-5 * 6
+    assert rel_l2(est.inverse_transform(Y), g["Xback"]) <= 1e-5 * 6
+
+
+def test_estimator_round_trips_and_params(cuda):
+    X = signals(3, 128)
+    est = sf.FourierTransformer().fit(X)
+    assert rel_l2(est.inverse_transform(est.transform(X)), X) <= 1e-4
+    X = signals(2, 32, seed=5)
+    mixed = sf.FourierTransformer(algorithm="mixed").fit_transform(X)
+    split = sf.FourierTransformer(algorithm="split").fit_transform(X)
+    assert rel_l2(mixed, split) <= 1e-4
+    X = signals(2, 16, seed=6)
+    back = sf.FourierTransformer().fit(X).transform(sf.FourierTransformer(direction="inverse").fit(X).transform(X))
+    assert rel_l2(back, X) <= 1e-4
+    est = sf.FourierTransformer().fit(signals(2, 64))
+    with pytest.raises(sf.ShapeError):
+        est.transform(signals(2, 32))
+    from sklearn.pipeline import Pipeline
+
+    assert Pipeline([("fft", sf.FourierTransformer())]).fit_transform(signals(4, 8)).shape == (4, 8)
+    Xd = sf.generate_batch(7, 2048, seed=1, precision="double")
+    yd = sf.FourierTransformer(precision="double").fit_transform(torch.from_numpy(Xd).to(cuda))
+    assert row_rel_l2(yd.cpu().numpy(), oracle.direct_dft(Xd)).max() <= 1e-13 * 11
+
+
+def test_execute_timed(cuda):
+    plan = sf.make_plan(512)
+    x = sf.generate("ramp", 512)
+    timed = sf.execute_timed(plan, x)
+    assert np.array_equal(timed.output, sf.execute(plan, x))
+    assert timed.dispatch_us >= 0.0 and timed.compute_us > 0.0
+    xt = torch.from_numpy(sf.generate_batch(1000, 512, seed=2)).to(cuda)
+    t2 = sf.execute_timed(plan, xt)
+    assert torch.equal(t2.output, sf.execute(plan, xt)) and t2.compute_us > 0
+    t3 = sf.execute_timed(sf.make_plan(2048), sf.generate("ramp", 2048))
+    assert t3.compute_us < 50_000  # reference soft guard (test_executor.py:121-127)
+
+
+def test_criterion_01_oracle_sweep(cuda):
+    worst = 0.0
+    for n in ENGINE_N:
+        plan = sf.make_plan(n)
+        for kind in ("ramp", "impulse", "constant", "random"):
+            x = sf.generate(kind, n, seed=0)
+            worst = max(worst, rel_l2(sf.execute(plan, x), oracle.direct_dft(x)))
+    assert worst <= 1e-4
+
+
+def test_criterion_04_round_trips_batched(cuda):
+    # 100 seeds per length and algorithm, as ONE batched launch per plan
+    for n in ENGINE_N:
+        x = np.stack([sf.generate("random", n, seed=s) for s in range(100)])
+        for alg in ("mixed", "split"):
+            fwd = sf.make_plan(n, "forward", alg)
+            inv = sf.make_plan(n, "inverse", alg)
+            assert row_rel_l2(sf.execute(inv, sf.execute(fwd, x)), x).max() <= 1e-4
+
+
+def test_criterion_05_parseval_linearity(cuda):
+    for n in (8, 64, 512, 2048):
+        plan = sf.make_plan(n)
+        rng = np.random.default_rng(n)
+        a = (rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)).astype(np.complex64)
+        b = (rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)).astype(np.complex64)
+        fa = sf.execute(plan, a).astype(np.complex128)
+        fb = sf.execute(plan, b).astype(np.complex128)
+        et = float(np.sum(np.abs(a.astype(np.complex128)) ** 2))
+        assert abs(et - float(np.sum(np.abs(fa) ** 2)) / n) / et <= 1e-4
+        al, be = 2.5 - 0.5j, -1.25 + 3.0j
+        mixed = sf.execute(plan, al * a + be * b).astype(np.complex128)
+        assert rel_l2(mixed, al * fa + be * fb) <= 1e-4
+
+
+def test_criterion_10_cross_plan_equivalence(cuda):
+    plans = [sf.make_plan(16, stages=[8, 2]), sf.make_plan(16, stages=[4, 4]),
+             sf.make_plan(16, stages=[2, 2, 2, 2]), sf.make_plan(16, algorithm="split")]
+    x = np.stack([sf.generate("random", 16, seed=s) for s in range(100)])
+    outs = [sf.execute(p, x) for p in plans]
+    for o in outs[1:]:
+        assert row_rel_l2(o, outs[0]).max() <= 1e-4
+
+
+def test_split_radix_transform_on_gpu(cuda, golden):
+    g = golden("engine_c64.npz")
+    for n in (2, 4, 8, 16, 64):
+        x = g[f"in_split_{n}"]
+        for d in ("forward", "inverse"):
+            y = sf.split_radix_transform(x, sf.build_twiddle_table(n), d, verify_twiddles=True)
+            assert rel_l2(y, g[f"out_split_{n}_{d}"]) <= 1e-5 * max(1, np.log2(n))
+
+
+def test_execute_sharded_matches_single_device(cuda):
+    x = sf.generate_batch(1001, 256, seed=4)
+    plan = sf.make_plan(256)
+    want = sf.execute(plan, x)
+    ndev = torch.cuda.device_count()
+    devices = list(range(ndev)) if ndev > 1 else [0, 0, 0]
+    assert np.array_equal(sf.execute_sharded(plan, x, devices), want)
+
+
+def test_large_full_size_properties(cuda):
+    """Config 2 at full size: round trip + Parseval over all 65536 rows on the GPU."""
+    n, b = 1024, 65536
+    x = torch.from_numpy(sf.generate_batch(b, n, seed=1)).to(cuda)
+    y = sf.execute(sf.make_plan(n), x)
+    back = sf.execute(sf.make_plan(n, "inverse"), y)
+    err = (torch.linalg.vector_norm(back - x, dim=1) / torch.linalg.vector_norm(x, dim=1)).max().item()
+    assert err <= 1e-5 * 10
+    ex = torch.sum(torch.abs(x.to(torch.complex128)) ** 2, dim=1)
+    ey = torch.sum(torch.abs(y.to(torch.complex128)) ** 2, dim=1) / n
+    assert ((ex - ey).abs() / ex).max().item() <= 1e-5
