@@ -147,6 +147,42 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside), "window": note}
 
 
+# ------------------------------------------------------------- host link
+def host_link_rates(dev, nbytes=256 << 20, reps=3):
+    """Pinned H2D / D2H copy rates alone and concurrently (GB/s each way).
+
+    The e2e leg moves its whole input H2D and output D2H through this link,
+    so (bytes_in + bytes_out) / (2 * concurrent rate) bounds its step time.
+    """
+    import torch
+
+    h_a = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_b = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize(dev)
+        return (time.perf_counter() - t) / reps
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_b.copy_(d_b, non_blocking=True)
+
+    h2d = nbytes / timed(lambda: d_a.copy_(h_a, non_blocking=True)) / 1e9
+    d2h = nbytes / timed(lambda: h_b.copy_(d_b, non_blocking=True)) / 1e9
+    bidir = nbytes / timed(both) / 1e9
+    return {"h2d_gbs": round(h2d, 1), "d2h_gbs": round(d2h, 1), "bidir_gbs_each_way": round(bidir, 1)}
+
+
 # -------------------------------------------------------------- CPU baseline
 def _cpu_worker(args):
     """Transform one resident chunk of rows ``reps`` times; returns (seconds, rows)."""
@@ -207,10 +243,16 @@ def run_gpu(args, n, batch, precision, direction, workload):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: run several ranks on one GPU (gloo for the scalar reduction)
+    local = int(os.environ.get("SFFT_BENCH_DEVICE", local))
+    backend = os.environ.get("SFFT_BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -286,6 +328,9 @@ def run_gpu(args, n, batch, precision, direction, workload):
     if rank == 0 and not args.no_check:
         assert np.array_equal(hout_np[:64], y[:64].cpu().numpy()), "e2e output differs from device output"
 
+    link = host_link_rates(dev)
+    link_bound_s = max(batch * rb / (link["bidir_gbs_each_way"] * 1e9),
+                       batch * rb / (link["h2d_gbs"] * 1e9) + 0.0)
     total_rows = batch * world
     fl = flops_per_row(n)
     value = total_rows * fl / (region_ms / args.steps * 1e-3) / 1e9
@@ -324,6 +369,10 @@ def run_gpu(args, n, batch, precision, direction, workload):
             "d2h_bytes_per_step": batch * rb,
             "path": "execute(plan, pinned numpy, out=pinned numpy) -> sfft_execute_host",
             "ms_per_step": round(e2e_s * 1e3, 3),
+            "bound": "host link (PCIe)",
+            "link": link,
+            "link_bound_ms_per_step": round(link_bound_s * 1e3, 3),
+            "frac_of_link_bound": round(link_bound_s / e2e_s, 4),
         },
         "roofline": {
             "bound": "hbm",

@@ -120,8 +120,18 @@ int sfft_plan_twiddles(sfft_plan_t plan, void* host_out, int64_t capacity_bytes)
 int sfft_execute(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch, void* stream,
                  int32_t* d_nonfinite);
 
+/* Synchronous execute on device memory with the reference's contract:
+ * launches on `stream`, waits for it, and returns SFFT_ERR_DOMAIN if any
+ * input value was NaN/Inf (checked through a pinned, mapped per-thread flag:
+ * no extra kernel or copy).  If `kernel_ms` is non-NULL it receives the
+ * kernel's device time from CUDA events recorded around the launch. */
+int sfft_execute_sync(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch,
+                      void* stream, float* kernel_ms);
+
 /* Synchronous execute on host memory: chunked H2D -> kernel -> D2H pipeline
- * over several streams (pinned memory gives full PCIe/C2C bandwidth).
+ * over several streams (pinned memory gives full PCIe/C2C bandwidth);
+ * calls up to 1 MiB take a single-stream latency path (pageable memory is
+ * bounced through a pinned buffer).
  * Returns SFFT_ERR_DOMAIN if the input held NaN/Inf (output then undefined). */
 int sfft_execute_host(sfft_plan_t plan, const void* h_in, void* h_out, int64_t batch);
 

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "sfft_variant_info",
     "sfft_plan_twiddles",
     "sfft_execute",
+    "sfft_execute_sync",
     "sfft_execute_host",
     "sfft_last_error",
 )
@@ -84,6 +85,7 @@ def _bind(lib):
         "sfft_plan_twiddles": ([p, p, i64], ctypes.c_int),
         "sfft_variant_info": ([i32, i32, i32, ctypes.POINTER(PlanInfo)], ctypes.c_int),
         "sfft_execute": ([p, p, p, i64, p, p], ctypes.c_int),
+        "sfft_execute_sync": ([p, p, p, i64, p, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
         "sfft_execute_host": ([p, p, p, i64], ctypes.c_int),
         "sfft_last_error": ([], ctypes.c_char_p),
     }

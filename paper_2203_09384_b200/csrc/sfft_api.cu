@@ -244,6 +244,48 @@ struct DeviceGuard {
 };
 
 constexpr int kHostStreams = 3;
+constexpr int64_t kSmallCallBytes = int64_t(1) << 20;  // single-stream fast path
+
+// Per-thread resources of the synchronous entry points: a pinned, mapped
+// non-finite flag (no memset kernel, no D2H copy to read it) and a pair of
+// timing events per device.
+struct ThreadSync {
+  int32_t* h_flag = nullptr;
+  int32_t* d_flag = nullptr;
+  int ev_device[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  cudaEvent_t ev[8][2] = {};
+  ~ThreadSync() {
+    if (h_flag) cudaFreeHost(h_flag);
+  }
+  cudaError_t flag() {
+    if (h_flag) return cudaSuccess;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h_flag), sizeof(int32_t),
+                                  cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_flag), h_flag, 0);
+    return e;
+  }
+  cudaError_t events(int device, cudaEvent_t** out) {
+    const int slot = device & 7;
+    if (ev_device[slot] != device) {
+      cudaError_t e = cudaEventCreate(&ev[slot][0]);
+      if (e == cudaSuccess) e = cudaEventCreate(&ev[slot][1]);
+      if (e != cudaSuccess) return e;
+      ev_device[slot] = device;
+    }
+    *out = ev[slot];
+    return cudaSuccess;
+  }
+};
+thread_local ThreadSync t_sync;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
 
 }  // namespace
 
@@ -260,7 +302,10 @@ struct sfft_plan {
   cudaStream_t streams[kHostStreams] = {};
   void* d_in[kHostStreams] = {};
   void* d_out[kHostStreams] = {};
-  int32_t* d_flag = nullptr;
+  int32_t* h_flag = nullptr;  // pinned + mapped: kernels OR into it, host reads it
+  int32_t* d_flag = nullptr;  // device alias of h_flag
+  unsigned char* h_stage = nullptr;  // pinned bounce buffer for small pageable calls
+  int64_t h_stage_bytes = 0;
 };
 
 extern "C" {
@@ -387,8 +432,9 @@ int sfft_plan_destroy(sfft_plan_t p) {
         cudaFree(p->d_out[i]);
         cudaStreamDestroy(p->streams[i]);
       }
-      cudaFree(p->d_flag);
+      cudaFreeHost(p->h_flag);
     }
+    if (p->h_stage) cudaFreeHost(p->h_stage);
   }
   delete p;
   return SFFT_OK;
@@ -467,6 +513,41 @@ int sfft_execute(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, vo
   return SFFT_OK;
 }
 
+int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                      float* kernel_ms) {
+  if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
+  if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
+  if (kernel_ms) *kernel_ms = 0.f;
+  if (batch == 0) return SFFT_OK;
+  if (d_in == nullptr || d_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
+  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)
+    return fail(SFFT_ERR_ARGUMENT, "data pointers must be 16-byte aligned");
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  cudaError_t e = t_sync.flag();
+  if (e != cudaSuccess) return cuda_fail(e, "flag allocation");
+  *t_sync.h_flag = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t* ev = nullptr;
+  if (kernel_ms) {
+    e = t_sync.events(p->device, &ev);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
+    if (e != cudaSuccess) return cuda_fail(e, "event record");
+  }
+  e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch, t_sync.d_flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (kernel_ms) {
+    e = cudaEventRecord(ev[1], st);
+    if (e != cudaSuccess) return cuda_fail(e, "event record");
+  }
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  if (kernel_ms) cudaEventElapsedTime(kernel_ms, ev[0], ev[1]);
+  if (*reinterpret_cast<volatile int32_t*>(t_sync.h_flag))
+    return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
+  return SFFT_OK;
+}
+
 int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch) {
   if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
   if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
@@ -480,7 +561,10 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   if (!p->host_ready) {
     for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i)
       e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_flag, sizeof(int32_t) * kHostStreams);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_flag), sizeof(int32_t) * kHostStreams,
+                        cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_flag), p->h_flag, 0);
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
     p->host_ready = true;
   }
@@ -504,33 +588,56 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
     p->host_chunk_rows = want_rows;
   }
-  e = cudaMemsetAsync(p->d_flag, 0, sizeof(int32_t) * kHostStreams, p->streams[0]);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->streams[0]);
-  if (e != cudaSuccess) return cuda_fail(e, "flag reset");
-  const unsigned char* src = static_cast<const unsigned char*>(h_in);
-  unsigned char* dst = static_cast<unsigned char*>(h_out);
-  int chunk = 0;
-  for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
-    const int s = chunk % kHostStreams;
-    const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
-    const size_t bytes = size_t(rows * row_bytes);
-    cudaStream_t st = p->streams[s];
-    e = cudaMemcpyAsync(p->d_in[s], src + row * row_bytes, bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-    e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, st);
-    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-    e = cudaMemcpyAsync(dst + row * row_bytes, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  for (int i = 0; i < kHostStreams; ++i) p->h_flag[i] = 0;
+  const int64_t total = batch * row_bytes;
+
+  if (total <= kSmallCallBytes) {
+    // latency path: one stream; pageable user memory goes through a pinned
+    // bounce buffer (a host memcpy is cheaper than the driver's staging)
+    const bool pinned = is_pinned(h_in) && is_pinned(h_out);
+    if (!pinned && p->h_stage == nullptr) {
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_stage), 2 * kSmallCallBytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_fail(e, "pinned staging allocation");
+      p->h_stage_bytes = 2 * kSmallCallBytes;
+    }
+    const void* src = h_in;
+    void* dst = h_out;
+    if (!pinned) {
+      std::memcpy(p->h_stage, h_in, size_t(total));
+      src = p->h_stage;
+      dst = p->h_stage + kSmallCallBytes;
+    }
+    cudaStream_t st = p->streams[0];
+    e = cudaMemcpyAsync(p->d_in[0], src, size_t(total), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = p->v->launch[p->direction](p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, p->d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
+    if (!pinned) std::memcpy(h_out, dst, size_t(total));
+  } else {
+    const unsigned char* src = static_cast<const unsigned char*>(h_in);
+    unsigned char* dst = static_cast<unsigned char*>(h_out);
+    int chunk = 0;
+    for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
+      const int s = chunk % kHostStreams;
+      const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
+      const size_t bytes = size_t(rows * row_bytes);
+      cudaStream_t st = p->streams[s];
+      e = cudaMemcpyAsync(p->d_in[s], src + row * row_bytes, bytes, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+      e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, st);
+      if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+      e = cudaMemcpyAsync(dst + row * row_bytes, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    }
+    for (int i = 0; i < kHostStreams; ++i) {
+      e = cudaStreamSynchronize(p->streams[i]);
+      if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+    }
   }
-  int32_t flags[kHostStreams] = {};
-  for (int i = 0; i < kHostStreams; ++i) {
-    e = cudaStreamSynchronize(p->streams[i]);
-    if (e != cudaSuccess) return cuda_fail(e, "stream sync");
-  }
-  e = cudaMemcpy(flags, p->d_flag, sizeof(flags), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return cuda_fail(e, "flag read");
   for (int i = 0; i < kHostStreams; ++i)
-    if (flags[i]) return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
+    if (reinterpret_cast<volatile int32_t*>(p->h_flag)[i])
+      return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
   return SFFT_OK;
 }
 

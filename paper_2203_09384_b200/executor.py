@@ -147,20 +147,22 @@ def _execute_device(plan: FftPlan, x, timed: bool = False, out=None):
         or out.data_ptr() % 16
     ):
         raise ShapeError("out must be a contiguous, 16-byte aligned tensor of the plan dtype on the input device")
-    flag = torch.zeros(1, dtype=torch.int32, device=xc.device)
     stream = torch.cuda.current_stream(xc.device)
-    if timed:
-        start = torch.cuda.Event(enable_timing=True)
-        stop = torch.cuda.Event(enable_timing=True)
-        start.record(stream)
+    handle = plan.native_handle(xc.device.index)
+    kernel_ms = ctypes.c_float(0.0)
     t1 = time.perf_counter_ns()
-    launch(plan, xc, out, rows, stream=stream, flag=flag)
-    if timed:
-        stop.record(stream)
-    if int(flag.item()):  # synchronises the stream
-        raise DomainError("signal contains NaN or Inf values")
-    compute_us = start.elapsed_time(stop) * 1000.0 if timed else 0.0
-    return out, (t1 - t0) / 1000.0, compute_us
+    # one C call: launch, wait, read the mapped NaN/Inf flag (DomainError)
+    _native.check(
+        _native.lib().sfft_execute_sync(
+            handle,
+            ctypes.c_void_p(xc.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()),
+            rows,
+            ctypes.c_void_p(stream.cuda_stream),
+            ctypes.byref(kernel_ms) if timed else None,
+        )
+    )
+    return out, (t1 - t0) / 1000.0, kernel_ms.value * 1000.0
 
 
 # ----------------------------------------------------------------- public API
@@ -183,7 +185,8 @@ def execute_timed(plan: FftPlan, signal) -> TimedExecution:
 
     ``dispatch_us``: host time from entry to the kernel launch (validation,
     dtype conversion and, for host input, the H2D copy); ``compute_us``: the
-    kernel's device time from CUDA events on the launch stream.
+    kernel's device time from CUDA events recorded around the launch on its
+    stream (sfft_execute_sync).
     """
     if _is_torch(signal) and signal.is_cuda:
         return TimedExecution(*_execute_device(plan, signal, timed=True))
