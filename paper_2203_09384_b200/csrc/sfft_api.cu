@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -243,7 +244,30 @@ struct DeviceGuard {
   }
 };
 
-constexpr int kHostStreams = 3;
+constexpr int kMaxHostStreams = 8;
+
+// Host pipeline shape: streams and chunk size (env SFFT_HOST_STREAMS /
+// SFFT_HOST_CHUNK_MB override the defaults, read once).
+struct HostPipelineShape {
+  // measured on the B200 host link (profiles/r01_e2e_sweep.jsonl): 32 MiB
+  // chunks reach ~97% of the concurrent H2D+D2H rate; streams >= 2 suffice
+  int streams = 3;
+  int64_t chunk_bytes = int64_t(32) << 20;
+  HostPipelineShape() {
+    if (const char* e = std::getenv("SFFT_HOST_STREAMS")) {
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= kMaxHostStreams) streams = v;
+    }
+    if (const char* e = std::getenv("SFFT_HOST_CHUNK_MB")) {
+      const long v = std::atol(e);
+      if (v >= 1 && v <= 1024) chunk_bytes = int64_t(v) << 20;
+    }
+  }
+};
+const HostPipelineShape& host_shape() {
+  static const HostPipelineShape shape;
+  return shape;
+}
 constexpr int64_t kSmallCallBytes = int64_t(1) << 20;  // single-stream fast path
 
 // Per-thread resources of the synchronous entry points: a pinned, mapped
@@ -299,9 +323,10 @@ struct sfft_plan {
   std::mutex host_mu;
   bool host_ready = false;
   int64_t host_chunk_rows = 0;
-  cudaStream_t streams[kHostStreams] = {};
-  void* d_in[kHostStreams] = {};
-  void* d_out[kHostStreams] = {};
+  int nstreams = 0;
+  cudaStream_t streams[kMaxHostStreams] = {};
+  void* d_in[kMaxHostStreams] = {};
+  void* d_out[kMaxHostStreams] = {};
   int32_t* h_flag = nullptr;  // pinned + mapped: kernels OR into it, host reads it
   int32_t* d_flag = nullptr;  // device alias of h_flag
   unsigned char* h_stage = nullptr;  // pinned bounce buffer for small pageable calls
@@ -426,7 +451,7 @@ int sfft_plan_destroy(sfft_plan_t p) {
     DeviceGuard guard(p->device);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->host_ready) {
-      for (int i = 0; i < kHostStreams; ++i) {
+      for (int i = 0; i < p->nstreams; ++i) {
         cudaStreamSynchronize(p->streams[i]);
         cudaFree(p->d_in[i]);
         cudaFree(p->d_out[i]);
@@ -559,36 +584,38 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   const int64_t row_bytes = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
   cudaError_t e = cudaSuccess;
   if (!p->host_ready) {
-    for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i)
+    p->nstreams = host_shape().streams;
+    for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i)
       e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
     if (e == cudaSuccess)
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_flag), sizeof(int32_t) * kHostStreams,
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_flag), sizeof(int32_t) * kMaxHostStreams,
                         cudaHostAllocMapped | cudaHostAllocPortable);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_flag), p->h_flag, 0);
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
     p->host_ready = true;
   }
-  // 16 MiB chunks: large enough for full-rate DMA, small enough to overlap
-  // copies in both directions with the kernels of neighbouring chunks.
+  // chunks large enough for full-rate DMA, small enough to overlap copies in
+  // both directions with the kernels of neighbouring chunks.
   // Staging buffers grow on demand, so small calls stay small.
-  const int64_t max_chunk_rows = (int64_t(16) << 20) / row_bytes > 0 ? (int64_t(16) << 20) / row_bytes : 1;
+  const int64_t chunk_bytes = host_shape().chunk_bytes;
+  const int64_t max_chunk_rows = chunk_bytes / row_bytes > 0 ? chunk_bytes / row_bytes : 1;
   const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
   if (want_rows > p->host_chunk_rows) {
-    for (int i = 0; i < kHostStreams; ++i) {
+    for (int i = 0; i < p->nstreams; ++i) {
       cudaStreamSynchronize(p->streams[i]);
       cudaFree(p->d_in[i]);
       cudaFree(p->d_out[i]);
       p->d_in[i] = p->d_out[i] = nullptr;
     }
     p->host_chunk_rows = 0;
-    for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i) {
+    for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i) {
       e = cudaMalloc(&p->d_in[i], want_rows * row_bytes);
       if (e == cudaSuccess) e = cudaMalloc(&p->d_out[i], want_rows * row_bytes);
     }
     if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
     p->host_chunk_rows = want_rows;
   }
-  for (int i = 0; i < kHostStreams; ++i) p->h_flag[i] = 0;
+  for (int i = 0; i < kMaxHostStreams; ++i) p->h_flag[i] = 0;
   const int64_t total = batch * row_bytes;
 
   if (total <= kSmallCallBytes) {
@@ -619,7 +646,7 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     unsigned char* dst = static_cast<unsigned char*>(h_out);
     int chunk = 0;
     for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
-      const int s = chunk % kHostStreams;
+      const int s = chunk % p->nstreams;
       const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
       const size_t bytes = size_t(rows * row_bytes);
       cudaStream_t st = p->streams[s];
@@ -630,12 +657,12 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
       e = cudaMemcpyAsync(dst + row * row_bytes, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
     }
-    for (int i = 0; i < kHostStreams; ++i) {
+    for (int i = 0; i < p->nstreams; ++i) {
       e = cudaStreamSynchronize(p->streams[i]);
       if (e != cudaSuccess) return cuda_fail(e, "stream sync");
     }
   }
-  for (int i = 0; i < kHostStreams; ++i)
+  for (int i = 0; i < kMaxHostStreams; ++i)
     if (reinterpret_cast<volatile int32_t*>(p->h_flag)[i])
       return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
   return SFFT_OK;
