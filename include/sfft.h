@@ -135,6 +135,22 @@ int sfft_execute_sync(sfft_plan_t plan, const void* d_in, void* d_out, int64_t b
  * Returns SFFT_ERR_DOMAIN if the input held NaN/Inf (output then undefined). */
 int sfft_execute_host(sfft_plan_t plan, const void* h_in, void* h_out, int64_t batch);
 
+/* Stage-level API (kernels.py:28-151, planner.py:62-89) on device buffers --
+ * not the hot path (that is sfft_execute: all stages fused in one HBM pass),
+ * but the reference's building blocks for custom stage lists.
+ *
+ * sfft_permute: out[r, p] = in[r, perm[p]] for `batch` rows of n elements
+ *   (the digit-reversal load of executor.py:77); perm is int64 on device.
+ * sfft_stage: one out-of-place radix-2/4/8 decimation-in-time stage over
+ *   sub-spectra of length `stride`; operand (q, j) of each group is scaled
+ *   by table[(n/(radix*stride))*q*j mod n] (conjugated for SFFT_INVERSE);
+ *   `d_table` is the n-entry base table of sfft_build_twiddle_table on the
+ *   device.  SFFT_ERR_PLAN if radix*stride does not divide n. */
+int sfft_permute(int32_t n, int32_t precision, const int64_t* d_perm, const void* d_in,
+                 void* d_out, int64_t batch, void* stream);
+int sfft_stage(int32_t n, int32_t precision, int32_t radix, int32_t stride, int32_t direction,
+               const void* d_table, const void* d_in, void* d_out, int64_t batch, void* stream);
+
 /* Thread-local message describing the last non-OK status on this thread. */
 const char* sfft_last_error(void);
 

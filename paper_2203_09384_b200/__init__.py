@@ -38,6 +38,7 @@ from .planner import (
 )
 from . import sharding
 from .sharding import execute_sharded, max_over_ranks, shard_bounds
+from .stages import StageBuffer, digit_reverse, radix2_stage, radix4_stage, radix8_stage
 from .signalgen import KINDS, generate, generate_batch
 
 try:
@@ -65,6 +66,7 @@ __all__ = [
     "Precision",
     "SUPPORTED_LENGTHS",
     "SUPPORTED_RADICES",
+    "StageBuffer",
     "ShapeError",
     "TABLE_MAX_LENGTH",
     "TimedExecution",
@@ -72,6 +74,7 @@ __all__ = [
     "UnsupportedLengthError",
     "build_twiddle_table",
     "count_butterflies",
+    "digit_reverse",
     "digit_reversal_permutation",
     "execute",
     "execute_sharded",
@@ -82,6 +85,9 @@ __all__ = [
     "is_power_of_two",
     "launch",
     "make_plan",
+    "radix2_stage",
+    "radix4_stage",
+    "radix8_stage",
     "max_over_ranks",
     "shard_bounds",
     "split_radix_transform",

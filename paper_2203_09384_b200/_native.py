@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "sfft_execute",
     "sfft_execute_sync",
     "sfft_execute_host",
+    "sfft_permute",
+    "sfft_stage",
     "sfft_last_error",
 )
 
@@ -87,6 +89,8 @@ def _bind(lib):
         "sfft_execute": ([p, p, p, i64, p, p], ctypes.c_int),
         "sfft_execute_sync": ([p, p, p, i64, p, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
         "sfft_execute_host": ([p, p, p, i64], ctypes.c_int),
+        "sfft_permute": ([i32, i32, p, p, p, i64, p], ctypes.c_int),
+        "sfft_stage": ([i32, i32, i32, i32, i32, p, p, p, i64, p], ctypes.c_int),
         "sfft_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():

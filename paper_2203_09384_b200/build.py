@@ -18,8 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libsfft.so")
-SOURCES = ["sfft_api.cu"]
-DEPS = ["sfft_api.cu", "sfft_kernels.cuh", "sfft_device.cuh"]
+SOURCES = ["sfft_api.cu", "sfft_stage.cu"]
+DEPS = ["sfft_api.cu", "sfft_stage.cu", "sfft_kernels.cuh", "sfft_device.cuh", "sfft_internal.h"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -3,7 +3,6 @@
 // reference interfaces each entry point replaces.
 #include <cuda_runtime.h>
 
-#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +13,7 @@
 #include <vector>
 
 #include "../../include/sfft.h"
+#include "sfft_internal.h"
 #include "sfft_kernels.cuh"
 
 namespace {
@@ -24,6 +24,12 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+}  // namespace
+
+int sfft_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
 
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(SFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));

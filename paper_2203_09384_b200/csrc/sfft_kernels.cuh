@@ -244,11 +244,10 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
       // last pass: output index b + q*L == j + m*G -> coalesced store
       if (valid) {
         C* dst = out + seq * N + j;
-        constexpr T scale = INV ? T(1) / T(N) : T(1);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
           C y = v[m];
-          if constexpr (INV) y = cscale(cswap(y), scale);
+          if constexpr (INV) y = cscale(cswap(y), T(1) / T(N));  // exact: N = 2^k
           st_stream(dst + m * G, y);
         }
       }
