@@ -235,3 +235,27 @@ def test_plan_info_and_twiddles(cuda):
     sf._native.check(sf._native.lib().sfft_plan_twiddles(plan.native_handle(0), buf.ctypes.data, buf.nbytes))
     assert np.array_equal(buf, plan.twiddles.factors)
     assert ctypes is not None
+
+
+@pytest.mark.parametrize("prec,n", [("single", 2), ("single", 1024), ("double", 2048)])
+def test_more_than_2_31_elements(cuda, prec, n):
+    """64-bit indexing: a batch with > 2^31 complex elements (16-32 GiB each way)."""
+    elems = (1 << 31) + 4096
+    batch = elems // n + 3
+    cdt = torch.complex64 if prec == "single" else torch.complex128
+    free, _ = torch.cuda.mem_get_info()
+    need = 2 * batch * n * (8 if prec == "single" else 16)
+    if need > 0.8 * free:
+        pytest.skip("not enough device memory")
+    x = torch.empty((batch, n), dtype=cdt, device=cuda)
+    x.real.uniform_(-1, 1)
+    x.imag.uniform_(-1, 1)
+    plan = sf.make_plan(n, precision=prec)
+    y = torch.empty_like(x)
+    sf.launch(plan, x, y, batch)
+    rows = [0, 1, batch // 2, batch - 2, batch - 1]
+    xs = x[rows].cpu().numpy()
+    got = y[rows].cpu().numpy()
+    del x, y
+    torch.cuda.empty_cache()
+    assert row_rel_l2(got, oracle.direct_dft(xs)).max() <= tolerance(n, prec)
