@@ -274,6 +274,11 @@ def run_gpu(args, n, batch, precision, direction, workload):
     cdt = torch.complex64 if precision == "single" else torch.complex128
     ndt = np.complex64 if precision == "single" else np.complex128
     rb = row_bytes(n, precision)
+    global_batch = batch * world
+    if args.scaling == "strong":  # fixed total work, contiguous row shards
+        global_batch = batch
+        lo, hi = sf.shard_bounds(batch, world, rank)
+        batch = max(1, hi - lo)
     plan = sf.make_plan(n, direction, precision=precision)
 
     # inputs: Philox rows (seeded per rank) in pinned host memory, then HBM
@@ -341,7 +346,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
     link = host_link_rates(dev)
     link_bound_s = max(batch * rb / (link["bidir_gbs_each_way"] * 1e9),
                        batch * rb / (link["h2d_gbs"] * 1e9) + 0.0)
-    total_rows = batch * world
+    total_rows = global_batch
     fl = flops_per_row(n)
     value = total_rows * fl / (region_ms / args.steps * 1e-3) / 1e9
     e2e_value = total_rows * fl / e2e_s / 1e9
@@ -357,7 +362,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
         "warmup": args.warmup,
         "ms_per_step": round(region_ms / args.steps, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "c64 (fp32)" if precision == "single" else "c128 (fp64)",
         "data": "synthetic Philox-uniform complex rows (signalgen random kind), seeded per rank",
@@ -470,6 +475,8 @@ def main():
     ap.add_argument("--precision", choices=["single", "double"])
     ap.add_argument("--direction", choices=["forward", "inverse"])
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: --batch rows per GPU (default); strong: --batch rows split across GPUs")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")

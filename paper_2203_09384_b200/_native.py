@@ -107,11 +107,18 @@ def lib():
         with _lock:
             if _lib is None:
                 if not os.path.exists(LIB_PATH):
-                    raise FftError(
-                        f"native library {LIB_PATH} is missing; build it with "
-                        "`python -c 'import __graft_entry__ as g; g.build()'` "
-                        "(there is no CPU fallback)"
-                    )
+                    # a fresh checkout: compile the sm_100a library in-tree
+                    # (nvcc is part of the image); never substitute a CPU path
+                    try:
+                        from .build import build
+
+                        build()
+                    except Exception as exc:  # noqa: BLE001
+                        raise FftError(
+                            f"native library {LIB_PATH} is missing and could not be built ({exc}); "
+                            "build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                            "(there is no CPU fallback)"
+                        ) from exc
                 _lib = _bind(ctypes.CDLL(LIB_PATH))
     return _lib
 

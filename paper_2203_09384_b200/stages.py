@@ -120,7 +120,7 @@ def digit_reverse(x, stages, precision: str = "single"):
     """``work[..., p] = x[..., perm[p]]`` on the GPU (executor.py:77 with planner.py:62-89)."""
     torch = _torch()
     dtype = np.complex64 if precision == "single" else np.complex128
-    perm = torch.from_numpy(np.asarray(digit_reversal_permutation(stages), dtype=np.int64)).cuda()
+    perm = torch.from_numpy(np.array(digit_reversal_permutation(stages), dtype=np.int64)).cuda()
     xd = _to_device(x, dtype)
     n = int(xd.shape[-1])
     if perm.numel() != n:
