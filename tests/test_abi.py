@@ -127,3 +127,57 @@ def test_no_gpu_means_loud_cuda_error():
 
     with pytest.raises(sf.CudaError):
         sf.execute(sf.make_plan(64), np.ones(64, np.complex64))
+
+
+C_GPU_CLIENT = r"""
+#include <complex.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include "sfft.h"
+/* plain-C caller: plan, host execute, compare with a direct DFT in double */
+int main(void) {
+  const int n = 256, batch = 33;
+  float* x = malloc(sizeof(float) * 2 * n * batch);
+  float* y = malloc(sizeof(float) * 2 * n * batch);
+  for (int i = 0; i < 2 * n * batch; ++i) x[i] = (float)((i * 7919 % 1000) / 500.0 - 1.0);
+  sfft_plan_t plan;
+  int rc = sfft_plan_create(&plan, n, SFFT_SINGLE, SFFT_FORWARD, batch, 0);
+  if (rc) { printf("create %d %s\n", rc, sfft_last_error()); return 1; }
+  rc = sfft_execute_host(plan, x, y, batch);
+  if (rc) { printf("execute %d %s\n", rc, sfft_last_error()); return 1; }
+  double worst = 0;
+  for (int b = 0; b < batch; b += 8) {
+    double num = 0, den = 0;
+    for (int k = 0; k < n; ++k) {
+      double complex acc = 0;
+      for (int m = 0; m < n; ++m) {
+        double a = -2.0 * M_PI * (double)((long)k * m % n) / n;
+        acc += (x[2 * (b * n + m)] + I * x[2 * (b * n + m) + 1]) * cexp(I * a);
+      }
+      double complex got = y[2 * (b * n + k)] + I * y[2 * (b * n + k) + 1];
+      num += pow(cabs(got - acc), 2); den += pow(cabs(acc), 2);
+    }
+    if (sqrt(num / den) > worst) worst = sqrt(num / den);
+  }
+  x[5] = NAN;
+  int dom = sfft_execute_host(plan, x, y, batch);
+  sfft_plan_destroy(plan);
+  printf("%.3e %d\n", worst, dom);
+  return worst < 8e-5 && dom == SFFT_ERR_DOMAIN ? 0 : 2;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_plain_c_client_on_gpu(tmp_path, cuda):
+    src = tmp_path / "gpu_client.c"
+    src.write_text(C_GPU_CLIENT)
+    exe = tmp_path / "gpu_client"
+    subprocess.run(
+        ["gcc", "-std=gnu99", "-O2", str(src), "-I", os.path.join(ROOT, "include"), "-L", _native.LIB_DIR,
+         "-lsfft", f"-Wl,-rpath,{_native.LIB_DIR}", "-lm", "-o", str(exe)],
+        check=True,
+    )
+    res = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout + res.stderr
