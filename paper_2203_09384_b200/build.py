@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libsfft.so")
 SOURCES = ["sfft_api.cu", "sfft_stage.cu"]
-DEPS = ["sfft_api.cu", "sfft_stage.cu", "sfft_kernels.cuh", "sfft_device.cuh", "sfft_internal.h"]
+DEPS = ["sfft_api.cu", "sfft_stage.cu", "sfft_kernels.cuh", "sfft_device.cuh", "sfft_internal.h", "host_copy.h"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/sfft.h"
+#include "host_copy.h"
 #include "sfft_internal.h"
 #include "sfft_kernels.cuh"
 
@@ -337,6 +338,11 @@ struct sfft_plan {
   int32_t* d_flag = nullptr;  // device alias of h_flag
   unsigned char* h_stage = nullptr;  // pinned bounce buffer for small pageable calls
   int64_t h_stage_bytes = 0;
+  // pinned per-slot chunk staging for large pageable calls
+  unsigned char* h_chunk_in[kMaxHostStreams] = {};
+  unsigned char* h_chunk_out[kMaxHostStreams] = {};
+  int64_t h_chunk_bytes = 0;
+  cudaEvent_t slot_done[kMaxHostStreams] = {};
 };
 
 extern "C" {
@@ -464,6 +470,11 @@ int sfft_plan_destroy(sfft_plan_t p) {
         cudaStreamDestroy(p->streams[i]);
       }
       cudaFreeHost(p->h_flag);
+      for (int i = 0; i < kMaxHostStreams; ++i) {
+        if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
+        if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
+        if (p->slot_done[i]) cudaEventDestroy(p->slot_done[i]);
+      }
     }
     if (p->h_stage) cudaFreeHost(p->h_stage);
   }
@@ -650,18 +661,73 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   } else {
     const unsigned char* src = static_cast<const unsigned char*>(h_in);
     unsigned char* dst = static_cast<unsigned char*>(h_out);
+    const bool pinned = is_pinned(h_in) && is_pinned(h_out);
+    const int64_t stage_bytes = p->host_chunk_rows * row_bytes;
+    if (!pinned && p->h_chunk_bytes < stage_bytes) {
+      for (int i = 0; i < p->nstreams; ++i) {
+        cudaStreamSynchronize(p->streams[i]);
+        if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
+        if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
+        p->h_chunk_in[i] = p->h_chunk_out[i] = nullptr;
+      }
+      p->h_chunk_bytes = 0;
+      for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i) {
+        e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_in[i]), stage_bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess)
+          e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_out[i]), stage_bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess && p->slot_done[i] == nullptr)
+          e = cudaEventCreateWithFlags(&p->slot_done[i], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "pinned chunk staging allocation");
+      p->h_chunk_bytes = stage_bytes;
+    }
+    auto& pool = sfft_host::CopyPool::instance();
+    // chunk bookkeeping for the staged (pageable) path: slot -> (row, rows)
+    int64_t slot_row[kMaxHostStreams] = {}, slot_rows[kMaxHostStreams] = {};
+    for (int i = 0; i < kMaxHostStreams; ++i) slot_rows[i] = 0;
+    auto drain_slot = [&](int s) -> cudaError_t {
+      if (slot_rows[s] == 0) return cudaSuccess;
+      const cudaError_t err = cudaEventSynchronize(p->slot_done[s]);
+      if (err != cudaSuccess) return err;
+      pool.memcpy(dst + slot_row[s] * row_bytes, p->h_chunk_out[s], size_t(slot_rows[s] * row_bytes));
+      slot_rows[s] = 0;
+      return cudaSuccess;
+    };
     int chunk = 0;
     for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
       const int s = chunk % p->nstreams;
       const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
       const size_t bytes = size_t(rows * row_bytes);
       cudaStream_t st = p->streams[s];
-      e = cudaMemcpyAsync(p->d_in[s], src + row * row_bytes, bytes, cudaMemcpyHostToDevice, st);
+      const void* h2d_src = src + row * row_bytes;
+      void* d2h_dst = dst + row * row_bytes;
+      if (!pinned) {
+        // the slot's previous chunk must have left the staging buffers
+        e = drain_slot(s);
+        if (e != cudaSuccess) return cuda_fail(e, "staging drain");
+        pool.memcpy(p->h_chunk_in[s], src + row * row_bytes, bytes);
+        h2d_src = p->h_chunk_in[s];
+        d2h_dst = p->h_chunk_out[s];
+      }
+      e = cudaMemcpyAsync(p->d_in[s], h2d_src, bytes, cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
       e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, st);
       if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-      e = cudaMemcpyAsync(dst + row * row_bytes, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
+      e = cudaMemcpyAsync(d2h_dst, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+      if (!pinned) {
+        e = cudaEventRecord(p->slot_done[s], st);
+        if (e != cudaSuccess) return cuda_fail(e, "event record");
+        slot_row[s] = row;
+        slot_rows[s] = rows;
+      }
+    }
+    if (!pinned) {
+      // drain in chunk order (oldest first)
+      for (int k = 0; k < p->nstreams; ++k) {
+        e = drain_slot((chunk + k) % p->nstreams);
+        if (e != cudaSuccess) return cuda_fail(e, "staging drain");
+      }
     }
     for (int i = 0; i < p->nstreams; ++i) {
       e = cudaStreamSynchronize(p->streams[i]);
