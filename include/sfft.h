@@ -72,7 +72,7 @@ typedef struct sfft_plan_info {
   int32_t variant;             /* index into the kernel variant table */
   int32_t layout;              /* stockham smem layout: 0 xor swizzle, 1 padded */
   int32_t twiddle_policy;      /* 0: every twiddle loaded; 1: powers of two + products */
-  int32_t reserved;
+  int32_t loader;              /* 0: per-thread global loads; 1: one bulk TMA copy per CTA */
 } sfft_plan_info_t;
 
 /* Library version (major*10000 + minor*100 + patch). */

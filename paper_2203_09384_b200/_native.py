@@ -61,7 +61,7 @@ class PlanInfo(ctypes.Structure):
         ("variant", ctypes.c_int32),
         ("layout", ctypes.c_int32),
         ("twiddle_policy", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("loader", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

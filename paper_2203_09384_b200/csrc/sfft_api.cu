@@ -46,6 +46,7 @@ struct Variant {
   int seq;         // sequences per CTA
   int layout;      // smem layout (stockham): 0 xor swizzle, 1 padded
   int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products
+  int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA
   int threads;     // threads per CTA
   int smem;        // dynamic smem bytes
   int passes;
@@ -61,7 +62,7 @@ constexpr int stockham_smem() {
   return SEQ * sfft::Smem<T, LAYOUT, R>::size(N) * int(sizeof(sfft::cx_t<T>));
 }
 
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
 cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
                             cudaStream_t st) {
   using C = sfft::cx_t<T>;
@@ -69,13 +70,13 @@ cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long
   constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   const long long grid = (batch + SEQ - 1) / SEQ;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP><<<dim3(unsigned(grid)), threads, smem, st>>>(
+  sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER><<<dim3(unsigned(grid)), threads, smem, st>>>(
       static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
   return cudaGetLastError();
 }
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
 cudaError_t prepare_stockham() {
-  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP>,
+  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               stockham_smem<T, N, R, SEQ, LAYOUT>());
 }
@@ -104,7 +105,7 @@ cudaError_t prepare_tile() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-template <typename T, int N, int R, int SEQ, int LAYOUT = 0, int TWP = 0>
+template <typename T, int N, int R, int SEQ, int LAYOUT = 0, int TWP = 0, int LOADER = 0>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
@@ -117,10 +118,11 @@ Variant stockham_variant() {
   for (int p = 0; p < v.passes && p < 8; ++p) v.radices[p] = sfft::pass_radix(N, R, p);
   v.tw_len = sfft::twiddle_table_len(N, R);
   v.twp = TWP;
-  v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP>;
-  v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP>;
-  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP>;
-  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP>;
+  v.loader = LOADER;
+  v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
+  v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
+  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
+  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   return v;
 }
 
@@ -159,13 +161,15 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {stockham_variant<float, 128, 16, 16, 0>(), stockham_variant<float, 128, 16, 16, 1>(),
            stockham_variant<float, 128, 8, 8, 1>()},
           {stockham_variant<float, 256, 16, 8, 1>(), stockham_variant<float, 256, 16, 8, 0>(),
-           stockham_variant<float, 256, 16, 8, 1, 1>()},
+           stockham_variant<float, 256, 16, 8, 1, 1>(), stockham_variant<float, 256, 16, 8, 1, 0, 1>()},
           {stockham_variant<float, 512, 16, 4, 1, 1>(), stockham_variant<float, 512, 16, 2, 1>(),
            stockham_variant<float, 512, 16, 4, 1>()},
-          {stockham_variant<float, 1024, 16, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1>(),
-           stockham_variant<float, 1024, 32, 4, 1>(), stockham_variant<float, 1024, 16, 2, 1>()},
+          {stockham_variant<float, 1024, 16, 1, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1, 1>(),
+           stockham_variant<float, 1024, 16, 1, 1>(), stockham_variant<float, 1024, 32, 4, 1>(),
+           stockham_variant<float, 1024, 16, 2, 1>(), stockham_variant<float, 1024, 16, 2, 1, 1, 1>()},
           {stockham_variant<float, 2048, 16, 1, 1, 1>(), stockham_variant<float, 2048, 16, 1, 1>(),
-           stockham_variant<float, 2048, 16, 1, 0>(), stockham_variant<float, 2048, 32, 1, 1>()},
+           stockham_variant<float, 2048, 16, 1, 0>(), stockham_variant<float, 2048, 32, 1, 1>(),
+           stockham_variant<float, 2048, 16, 1, 1, 1, 1>()},
       },
       {
           {},
@@ -181,9 +185,11 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {stockham_variant<double, 512, 16, 4, 0, 1>(), stockham_variant<double, 512, 16, 2, 0>(),
            stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 0>()},
           {stockham_variant<double, 1024, 16, 2, 0, 1>(), stockham_variant<double, 1024, 16, 1, 0, 1>(),
-           stockham_variant<double, 1024, 16, 1, 0>(), stockham_variant<double, 1024, 8, 1, 0>()},
+           stockham_variant<double, 1024, 16, 1, 0>(), stockham_variant<double, 1024, 8, 1, 0>(),
+           stockham_variant<double, 1024, 16, 2, 0, 1, 1>()},
           {stockham_variant<double, 2048, 16, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 0>(),
-           stockham_variant<double, 2048, 8, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 1>()},
+           stockham_variant<double, 2048, 8, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 1>(),
+           stockham_variant<double, 2048, 16, 1, 0, 1, 1>()},
       },
   };
   return table[precision][log2n];
@@ -501,6 +507,7 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   info->variant = p->variant;
   info->layout = p->v->layout;
   info->twiddle_policy = p->v->twp;
+  info->loader = p->v->loader;
   return SFFT_OK;
 }
 
@@ -527,6 +534,7 @@ int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_i
   info->variant = variant;
   info->layout = v.layout;
   info->twiddle_policy = v.twp;
+  info->loader = v.loader;
   return SFFT_OK;
 }
 

@@ -164,7 +164,45 @@ __device__ __forceinline__ void apply_pass_twiddles(C (&v)[R], const C* __restri
   }
 }
 
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
+// ------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// one bulk (1-D TMA) copy global -> shared, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+// LOADER 0: each thread loads its R elements straight into registers (LDG).
+// LOADER 1: one thread issues a single bulk TMA copy of the CTA's SEQ
+//           consecutive sequences (one contiguous byte range) into shared
+//           memory, the CTA waits on an mbarrier, and pass 0 gathers from
+//           shared memory -- no per-thread global loads at all.
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0>
 __global__ void __launch_bounds__((N / R) * SEQ)
 stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
                 const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
@@ -190,13 +228,35 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
   C* smq = LAYOUT == 1 ? sm + s * SN : sm;
 
   C v[R];
-  if (valid) {
-    const C* src = in + seq * N + j;
+  if constexpr (LOADER == 1) {
+    __shared__ __align__(8) unsigned long long bar;
+    const long long seq0 = (long long)blockIdx.x * SEQ;
+    const long long nseq = batch - seq0 < SEQ ? batch - seq0 : SEQ;
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      const uint32_t bytes = uint32_t(nseq * N * int(sizeof(C)));
+      mbar_expect_tx(&bar, bytes);
+      bulk_g2s(sm, in + seq0 * N, bytes, &bar);
+    }
+    __syncthreads();  // barrier initialised before anyone polls it
+    mbar_wait(&bar, 0);
+    if (valid) {
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+      for (int m = 0; m < R; ++m) v[m] = sm[s * N + j + m * G];  // linear staging, conflict-free
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
+    }
+    __syncthreads();  // staging fully read before the exchange layout reuses it
   } else {
+    if (valid) {
+      const C* src = in + seq * N + j;
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
+      for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
+    }
   }
   if (nonfinite != nullptr) {
     float2 acc = make_float2(0.f, 0.f);
