@@ -37,7 +37,33 @@ from .planner import (
     make_plan,
 )
 from . import sharding
+from .protocol import (
+    BenchmarkRecord,
+    BenchmarkResult,
+    BenchmarkSummary,
+    export_records,
+    export_summaries,
+    flag_outliers,
+    load_records,
+    run_benchmark,
+    summarize,
+)
 from .sharding import execute_sharded, max_over_ranks, shard_bounds
+from .sigio import read_signal, write_signal
+from .verify import (
+    ChiSquareReport,
+    Histogram,
+    build_histograms,
+    chi2_p_value,
+    chi2_reduced,
+    compare_spectra,
+    dft_matrix,
+    lower_regularized_gamma,
+    naive_dft,
+    relative_difference,
+    upper_regularized_gamma,
+    verify_batch,
+)
 from .stages import StageBuffer, digit_reverse, radix2_stage, radix4_stage, radix8_stage
 from .signalgen import KINDS, generate, generate_batch
 
@@ -51,6 +77,10 @@ __version__ = "0.1.0"
 __all__ = [
     "Algorithm",
     "ArgumentError",
+    "BenchmarkRecord",
+    "BenchmarkResult",
+    "BenchmarkSummary",
+    "ChiSquareReport",
     "CudaError",
     "Direction",
     "DomainError",
@@ -59,6 +89,7 @@ __all__ = [
     "FftError",
     "FftPlan",
     "FourierTransformer",
+    "Histogram",
     "InsufficientDataError",
     "InvalidLengthError",
     "KINDS",
@@ -66,30 +97,48 @@ __all__ = [
     "Precision",
     "SUPPORTED_LENGTHS",
     "SUPPORTED_RADICES",
-    "StageBuffer",
     "ShapeError",
+    "StageBuffer",
     "TABLE_MAX_LENGTH",
     "TimedExecution",
     "TwiddleTable",
     "UnsupportedLengthError",
+    "build_histograms",
     "build_twiddle_table",
+    "chi2_p_value",
+    "chi2_reduced",
+    "compare_spectra",
     "count_butterflies",
-    "digit_reverse",
+    "dft_matrix",
     "digit_reversal_permutation",
+    "digit_reverse",
     "execute",
     "execute_sharded",
     "execute_timed",
+    "export_records",
+    "export_summaries",
     "factorize_stages",
+    "flag_outliers",
     "generate",
     "generate_batch",
     "is_power_of_two",
     "launch",
+    "load_records",
+    "lower_regularized_gamma",
     "make_plan",
+    "max_over_ranks",
+    "naive_dft",
     "radix2_stage",
     "radix4_stage",
     "radix8_stage",
-    "max_over_ranks",
+    "read_signal",
+    "relative_difference",
+    "run_benchmark",
     "shard_bounds",
     "split_radix_transform",
+    "summarize",
     "twiddle",
+    "upper_regularized_gamma",
+    "verify_batch",
+    "write_signal",
 ]

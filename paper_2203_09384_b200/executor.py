@@ -9,8 +9,9 @@ may be shared by many threads -- and widens it:
   (executor.py:64-69);
 * numpy / array-like input runs through the native host pipeline
   (``sfft_execute_host``: chunked H2D -> kernel -> D2H) and returns numpy;
-  a torch CUDA tensor stays on its device (``sfft_execute`` on the current
-  stream) and returns a tensor there.
+  a torch CUDA tensor stays on its device (``sfft_execute_sync`` on the
+  current stream) and returns a tensor there; ``launch`` is the raw
+  asynchronous entry (``sfft_execute``) for pipelines that sync themselves.
 
 Every path launches the sm_100a kernels; there is no CPU fallback.  NaN/Inf
 input raises ``DomainError`` (executor.py:72-73) -- detected inside the kernel
