@@ -89,7 +89,7 @@ class ClockSampler:
     }
 
     def __init__(self, device_index: int, period_s: float = 0.002):
-        self.samples = []  # (t, sm_mhz, reasons_mask)
+        self.samples = []  # (t, sm_mhz, reasons_mask, power_w)
         self.period = period_s
         self.ok = False
         try:
@@ -126,7 +126,8 @@ class ClockSampler:
         nv = self.nvml
         while not self._stop.is_set():
             try:
-                self.samples.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), self._reasons()))
+                self.samples.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                     self._reasons(), nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
             except Exception:
                 pass
             time.sleep(self.period)
@@ -154,7 +155,8 @@ class ClockSampler:
             mask |= s[2]
         reasons = [name for bit, name in self.REASONS.items() if mask & bit and name != "gpu_idle"]
         return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(inside), "window": note}
+                "reasons": reasons, "samples": len(inside), "window": note,
+                "power_w": round(statistics.median(s[3] for s in inside), 1)}
 
 
 # ------------------------------------------------------------- host link

@@ -1,0 +1,11 @@
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,clocks.mem,power.draw,temperature.gpu,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/clocks14.csv &
+SMI=$!
+python tools/ab_variants.py 1024 single 65536 0,1,2,4 7
+python tools/ab_variants.py 1024 single 131072 0,1,2 7
+python tools/ab_variants.py 2048 single 65536 0,1,4 7
+python tools/ab_variants.py 2048 double 32768 0,1,4 7
+python tools/ab_variants.py 2048 double 131072 0,1,4 5
+python tools/ab_variants.py 1024 double 65536 0,1,4 7
+python tools/ab_variants.py 512 single 262144 0,1,2 7
+python tools/ab_variants.py 256 double 262144 0,1,2 7
+kill $SMI
