@@ -70,9 +70,12 @@ typedef struct sfft_plan_info {
   int32_t radices[8];          /* GPU pass radices, first to last */
   int64_t twiddle_elems;       /* per-pass twiddle table length (elements) */
   int32_t variant;             /* index into the kernel variant table */
-  int32_t layout;              /* stockham smem layout: 0 xor swizzle, 1 padded */
+  int32_t layout;              /* stockham smem layout: 1 padded, 2 row swizzle */
   int32_t twiddle_policy;      /* 0: every twiddle loaded; 1: powers of two + products */
-  int32_t loader;              /* 0: per-thread global loads; 1: one bulk TMA copy per CTA */
+  int32_t loader;              /* 0: per-thread global loads; 1: one bulk TMA copy per CTA;
+                                  2: persistent CTAs, pipelined bulk TMA copies */
+  int32_t smem_carveout;       /* preferred shared-memory carveout, % of max (-1: driver default) */
+  int32_t pipeline_stages;     /* loader 2: shared-memory stage buffers per CTA (else 0) */
 } sfft_plan_info_t;
 
 /* Library version (major*10000 + minor*100 + patch). */

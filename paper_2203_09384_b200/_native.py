@@ -62,6 +62,8 @@ class PlanInfo(ctypes.Structure):
         ("layout", ctypes.c_int32),
         ("twiddle_policy", ctypes.c_int32),
         ("loader", ctypes.c_int32),
+        ("smem_carveout", ctypes.c_int32),
+        ("pipeline_stages", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

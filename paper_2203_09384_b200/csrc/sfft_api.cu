@@ -38,7 +38,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 using LaunchFn = cudaError_t (*)(const void* in, void* out, const void* tw, long long batch,
                                  int* flag, cudaStream_t st);
-using PrepareFn = cudaError_t (*)();
+using PrepareFn = cudaError_t (*)(int carveout);
 
 struct Variant {
   int kernel;      // SFFT_KERNEL_*
@@ -46,7 +46,10 @@ struct Variant {
   int seq;         // sequences per CTA
   int layout;      // smem layout (stockham): 0 xor swizzle, 1 padded
   int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products
-  int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA
+  int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA,
+                   // 2 persistent CTAs with a `stages`-deep bulk TMA pipeline
+  int stages;      // loader 2: shared-memory stage buffers per CTA
+  int carveout;    // preferred shared-memory carveout, % of max (-1: driver default)
   int threads;     // threads per CTA
   int smem;        // dynamic smem bytes
   int passes;
@@ -75,10 +78,58 @@ cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long
   return cudaGetLastError();
 }
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
-cudaError_t prepare_stockham() {
-  return cudaFuncSetAttribute(sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              stockham_smem<T, N, R, SEQ, LAYOUT>());
+cudaError_t prepare_stockham(int carveout) {
+  const auto k = sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       stockham_smem<T, N, R, SEQ, LAYOUT>());
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+
+// ------------------------------------------------- persistent pipeline
+template <typename T, int N, int R, int SEQ, int LAYOUT, int STAGES>
+constexpr int pipe_smem() {
+  return STAGES * stockham_smem<T, N, R, SEQ, LAYOUT>();
+}
+
+// Resident CTAs of one kernel on one device, times its SM count: the
+// persistent grid.  Cached per kernel instantiation and device.
+template <typename K>
+int persistent_grid(K kernel, int threads, int smem) {
+  static int cached[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return 0;
+  if (cached[dev] > 0) return cached[dev];
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) return 0;
+  if (per_sm < 1) per_sm = 1;
+  cached[dev] = sms * per_sm;
+  return cached[dev];
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
+cudaError_t launch_stockham_pipe(const void* in, void* out, const void* tw, long long batch, int* flag,
+                                 cudaStream_t st) {
+  using C = sfft::cx_t<T>;
+  constexpr int threads = (N / R) * SEQ;
+  constexpr int smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
+  const auto k = sfft::stockham_pipe_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, STAGES>;
+  const long long tiles = (batch + SEQ - 1) / SEQ;
+  const int full = persistent_grid(k, threads, smem);
+  if (full <= 0) return cudaErrorInvalidConfiguration;
+  const long long grid = tiles < full ? tiles : full;
+  k<<<dim3(unsigned(grid)), threads, smem, st>>>(static_cast<const C*>(in), static_cast<C*>(out),
+                                                 static_cast<const C*>(tw), batch, flag);
+  return cudaGetLastError();
+}
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
+cudaError_t prepare_stockham_pipe(int carveout) {
+  const auto k = sfft::stockham_pipe_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>());
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
 }
 
 template <typename T>
@@ -99,13 +150,15 @@ cudaError_t launch_tile(const void* in, void* out, const void*, long long batch,
   return cudaGetLastError();
 }
 template <typename T, int N, int SPT, int W, bool INV>
-cudaError_t prepare_tile() {
+cudaError_t prepare_tile(int carveout) {
   constexpr int smem = tile_smem<T>(N, SPT, W);
-  return cudaFuncSetAttribute(sfft::tile_kernel<T, N, SPT, W, INV>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const auto k = sfft::tile_kernel<T, N, SPT, W, INV>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
 }
 
-template <typename T, int N, int R, int SEQ, int LAYOUT = 0, int TWP = 0, int LOADER = 0>
+template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
@@ -119,10 +172,33 @@ Variant stockham_variant() {
   v.tw_len = sfft::twiddle_table_len(N, R);
   v.twp = TWP;
   v.loader = LOADER;
+  // Per-thread global loads land in L1 before they reach registers, so every
+  // LDG line in flight holds L1 capacity.  Left to the driver, a variant
+  // whose resident CTAs fill the smem carveout (e.g. 12 x 16.9 KB -> 228 KB,
+  // 28 KB of L1) starves its own loads: 5.6 instead of 6.9-7.0 TB/s
+  // (tools/probe/occ_probe.cu, profiles/r01_occ_probe.txt).  Capping shared
+  // memory at half the unified 256 KB keeps >= 124 KB of L1.  Bulk (TMA)
+  // copies land in shared memory directly and keep the driver default.
+  v.carveout = LOADER == 0 ? 50 : -1;
   v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
+  return v;
+}
+
+// persistent pipelined Stockham (loader 2)
+template <typename T, int N, int R, int SEQ, int LAYOUT, int TWP, int STAGES>
+Variant pipe_variant() {
+  Variant v = stockham_variant<T, N, R, SEQ, LAYOUT, TWP, 1>();
+  v.loader = 2;
+  v.stages = STAGES;
+  v.smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
+  v.carveout = -1;  // bulk copies land in shared memory; the driver sizes it
+  v.launch[0] = &launch_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
+  v.launch[1] = &launch_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
+  v.prepare[0] = &prepare_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
+  v.prepare[1] = &prepare_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
   return v;
 }
 
@@ -137,6 +213,7 @@ Variant tile_variant() {
   v.passes = 1;
   v.radices[0] = N;
   v.tw_len = 0;
+  v.carveout = -1;  // cp.async stages through shared memory, not L1 lines
   v.launch[0] = &launch_tile<T, N, SPT, W, false>;
   v.launch[1] = &launch_tile<T, N, SPT, W, true>;
   v.prepare[0] = &prepare_tile<T, N, SPT, W, false>;
@@ -158,18 +235,19 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<float, 16, 2, 4>(), tile_variant<float, 16, 1, 8>()},
           {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32, 1>()},
           {stockham_variant<float, 64, 8, 16, 1>(), stockham_variant<float, 64, 16, 32, 1>()},
-          {stockham_variant<float, 128, 16, 16, 0>(), stockham_variant<float, 128, 16, 16, 1>(),
+          {stockham_variant<float, 128, 16, 16, 2>(), stockham_variant<float, 128, 16, 16, 1>(),
            stockham_variant<float, 128, 8, 8, 1>()},
-          {stockham_variant<float, 256, 16, 8, 1>(), stockham_variant<float, 256, 16, 8, 0>(),
+          {stockham_variant<float, 256, 16, 8, 1>(), stockham_variant<float, 256, 16, 8, 2>(),
            stockham_variant<float, 256, 16, 8, 1, 1>(), stockham_variant<float, 256, 16, 8, 1, 0, 1>()},
           {stockham_variant<float, 512, 16, 4, 1, 1>(), stockham_variant<float, 512, 16, 2, 1>(),
            stockham_variant<float, 512, 16, 4, 1>()},
           {stockham_variant<float, 1024, 32, 2, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1, 1, 1>(),
            stockham_variant<float, 1024, 16, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1>(),
            stockham_variant<float, 1024, 32, 4, 1>(), stockham_variant<float, 1024, 16, 2, 1>(),
-           stockham_variant<float, 1024, 16, 2, 1, 1, 1>(), stockham_variant<float, 1024, 32, 4, 1, 1>()},
+           stockham_variant<float, 1024, 16, 2, 1, 1, 1>(), stockham_variant<float, 1024, 32, 4, 1, 1>(),
+           pipe_variant<float, 1024, 16, 2, 1, 1, 3>()},
           {stockham_variant<float, 2048, 16, 1, 1, 1>(), stockham_variant<float, 2048, 16, 1, 1>(),
-           stockham_variant<float, 2048, 16, 1, 0>(), stockham_variant<float, 2048, 32, 1, 1>(),
+           stockham_variant<float, 2048, 16, 1, 2>(), stockham_variant<float, 2048, 32, 1, 1>(),
            stockham_variant<float, 2048, 16, 1, 1, 1, 1>(), stockham_variant<float, 2048, 32, 1, 1, 1>(),
            stockham_variant<float, 2048, 32, 2, 1, 1>()},
       },
@@ -178,20 +256,20 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<double, 2, 4, 4>(), tile_variant<double, 2, 2, 8>()},
           {tile_variant<double, 4, 2, 4>(), tile_variant<double, 4, 1, 8>()},
           {tile_variant<double, 8, 1, 4>(), tile_variant<double, 8, 2, 4>()},
-          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64, 0>()},
-          {stockham_variant<double, 32, 8, 32, 1>(), stockham_variant<double, 32, 8, 32, 0>()},
-          {stockham_variant<double, 64, 8, 16, 1>(), stockham_variant<double, 64, 8, 16, 0>()},
-          {stockham_variant<double, 128, 16, 16, 0>(), stockham_variant<double, 128, 8, 8, 1>()},
-          {stockham_variant<double, 256, 16, 8, 0, 1>(), stockham_variant<double, 256, 8, 4, 1>(),
-           stockham_variant<double, 256, 16, 8, 0>()},
-          {stockham_variant<double, 512, 16, 4, 0, 1>(), stockham_variant<double, 512, 16, 2, 0>(),
-           stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 0>()},
-          {stockham_variant<double, 1024, 16, 2, 0, 1>(), stockham_variant<double, 1024, 16, 1, 0, 1>(),
-           stockham_variant<double, 1024, 16, 1, 0>(), stockham_variant<double, 1024, 8, 1, 0>(),
-           stockham_variant<double, 1024, 16, 2, 0, 1, 1>()},
-          {stockham_variant<double, 2048, 16, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 0>(),
-           stockham_variant<double, 2048, 8, 1, 0, 1>(), stockham_variant<double, 2048, 16, 1, 1>(),
-           stockham_variant<double, 2048, 16, 1, 0, 1, 1>()},
+          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64, 2>()},
+          {stockham_variant<double, 32, 8, 32, 1>(), stockham_variant<double, 32, 8, 32, 2>()},
+          {stockham_variant<double, 64, 8, 16, 1>(), stockham_variant<double, 64, 8, 16, 2>()},
+          {stockham_variant<double, 128, 16, 16, 2>(), stockham_variant<double, 128, 8, 8, 1>()},
+          {stockham_variant<double, 256, 16, 8, 2, 1>(), stockham_variant<double, 256, 8, 4, 1>(),
+           stockham_variant<double, 256, 16, 8, 2>()},
+          {stockham_variant<double, 512, 16, 4, 2, 1>(), stockham_variant<double, 512, 16, 2, 2>(),
+           stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 2>()},
+          {stockham_variant<double, 1024, 16, 2, 2, 1>(), stockham_variant<double, 1024, 16, 1, 2, 1>(),
+           stockham_variant<double, 1024, 16, 1, 2>(), stockham_variant<double, 1024, 8, 1, 2>(),
+           stockham_variant<double, 1024, 16, 2, 2, 1, 1>()},
+          {stockham_variant<double, 2048, 16, 1, 2, 1>(), stockham_variant<double, 2048, 16, 1, 2>(),
+           stockham_variant<double, 2048, 8, 1, 2, 1>(), stockham_variant<double, 2048, 16, 1, 1>(),
+           stockham_variant<double, 2048, 16, 1, 2, 1, 1>(), pipe_variant<double, 2048, 16, 1, 2, 1, 3>()},
       },
   };
   return table[precision][log2n];
@@ -260,6 +338,17 @@ struct DeviceGuard {
 };
 
 constexpr int kMaxHostStreams = 8;
+
+// SFFT_SMEM_CARVEOUT (-1..100) overrides every variant's carveout (tuning).
+int carveout_override() {
+  static const int v = [] {
+    const char* e = std::getenv("SFFT_SMEM_CARVEOUT");
+    if (e == nullptr || *e == 0) return -2;
+    const int c = std::atoi(e);
+    return c >= -1 && c <= 100 ? c : -2;
+  }();
+  return v;
+}
 
 // Host pipeline shape: streams and chunk size (env SFFT_HOST_STREAMS /
 // SFFT_HOST_CHUNK_MB override the defaults, read once).
@@ -450,7 +539,7 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
       return cuda_fail(e, "twiddle upload");
     }
   }
-  e = p->v->prepare[direction]();
+  e = p->v->prepare[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
   if (e != cudaSuccess) {
     cudaFree(p->d_tw);
     delete p;
@@ -510,6 +599,8 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   info->layout = p->v->layout;
   info->twiddle_policy = p->v->twp;
   info->loader = p->v->loader;
+  info->smem_carveout = carveout_override() >= -1 ? carveout_override() : p->v->carveout;
+  info->pipeline_stages = p->v->stages;
   return SFFT_OK;
 }
 
@@ -537,6 +628,8 @@ int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_i
   info->layout = v.layout;
   info->twiddle_policy = v.twp;
   info->loader = v.loader;
+  info->smem_carveout = v.carveout;
+  info->pipeline_stages = v.stages;
   return SFFT_OK;
 }
 

@@ -7,8 +7,8 @@
 //   registers.  Pass 0 loads straight from HBM (lane j reads x[j + m*G]:
 //   consecutive lanes, consecutive addresses), every pass is a radix-r DFT in
 //   registers with per-pass twiddles from the plan's table, the exchange
-//   between passes goes through XOR-swizzled (bank-conflict-free) shared
-//   memory, and the last pass writes straight to HBM in natural order
+//   between passes goes through padded or row-swizzled (bank-conflict-free)
+//   shared memory, and the last pass writes straight to HBM in natural order
 //   (Stockham autosort: no digit-reversal gather, cf. executor.py:77).
 //   One HBM read + one HBM write per element.
 //
@@ -66,22 +66,32 @@ __host__ __device__ constexpr int twiddle_table_len(int n, int r) {
 // ------------------------------------------------------- smem layouts
 // Bank rows are 128 bytes = 16 fp32 / 8 fp64 complex; a warp access is served
 // per phase of 16 (8-byte) or 8 (16-byte) lanes.
-// LAYOUT 0: element XOR swizzle over the CTA-wide index.
 // LAYOUT 1: per-sequence region with one pad element after every R elements.
 //           Stride-R scatters become stride R+1 (odd), and addresses factor:
 //           map(base + c) = map(base) + c + c/R for c a multiple of R, so a
 //           pass's gathers are one base register plus immediate offsets.
+// LAYOUT 2: row swizzle over the CTA-wide index, e ^ ((e / R) & (W - 1)) with
+//           W = elements per bank row (needs R >= W).  The XOR only touches
+//           bits below log2 R, so for an offset c that is a multiple of R,
+//           map(base + c) = map'(base, (c / R) mod W) + c, and for an
+//           R-aligned base and c < R, map(base + c) = base + (c ^ term) --
+//           every access of a pass is one of <= W precomputed registers plus
+//           an immediate (no per-access shift/xor chain as in LAYOUT 0) and
+//           no padding (16-byte accesses stay 128-byte aligned per phase,
+//           which LAYOUT 1 breaks).
 // tests/test_bank_model.py replays every access of every variant per phase.
 template <typename T, int LAYOUT, int R>
 struct Smem {
+  static constexpr int W = sizeof(T) == 4 ? 16 : 8;  // complex elements per 128-byte row
+  static constexpr int LGR = ilog2(R);
+  static_assert(LAYOUT == 1 || LAYOUT == 2, "smem layout");
+  static_assert(LAYOUT != 2 || R >= W, "row swizzle needs R >= elements per bank row");
   __host__ __device__ static constexpr int size(int n) { return LAYOUT == 1 ? n + n / R : n; }
   __device__ static __forceinline__ int map(int e) {
     if constexpr (LAYOUT == 1) {
       return e + e / R;
-    } else if constexpr (sizeof(T) == 4) {
-      return e ^ (((e >> 4) ^ (e >> 8)) & 15);
     } else {
-      return e ^ (((e >> 3) ^ (e >> 6)) & 7);
+      return e ^ ((e >> LGR) & (W - 1));
     }
   }
   // map(base + off), off folds to a constant after unrolling; `base_aligned`
@@ -91,6 +101,10 @@ struct Smem {
     if constexpr (LAYOUT == 1) {
       if (off % R == 0) return mapped_base + off + off / R;
       if (base_aligned && off < R) return mapped_base + off;
+    } else if constexpr (LAYOUT == 2) {
+      // identical subexpressions per residue are CSE'd across the unrolled pass
+      if (off % R == 0) return (base ^ (((base >> LGR) + ((off >> LGR) & (W - 1))) & (W - 1))) + off;
+      if (base_aligned && off < R) return base + ((off & (W - 1)) ^ ((base >> LGR) & (W - 1))) + (off & ~(W - 1));
     }
     return map(base + off);
   }
@@ -125,13 +139,28 @@ __device__ __forceinline__ void seq_sync(int s) {
 }
 
 // ---------------------------------------------------------- Stockham kernel
-template <typename T>
-__device__ __forceinline__ void accumulate_nonfinite(float2& acc, uint32_t&, float2 v) {
-  acc = fma2(v, make_float2(0.f, 0.f), acc);  // Inf/NaN * 0 = NaN, sticky
+// Non-finite input check, one packed FFMA2 per complex element: Inf/NaN * 0
+// = NaN, sticky in `acc`.  fp64 feeds the high words reinterpreted as fp32:
+// a non-finite double has all-ones exponent bits 30..20, so its high word is
+// an fp32 Inf/NaN too -- as is the high word of a finite |x| >= 2^1017, which
+// is why a hit is re-checked exactly (nonfinite_exact) before it is reported.
+__device__ __forceinline__ void accumulate_nonfinite(float2& acc, float2 v) {
+  acc = fma2(v, make_float2(0.f, 0.f), acc);
 }
-template <typename T>
-__device__ __forceinline__ void accumulate_nonfinite(float2&, uint32_t& bad, double2 v) {
-  bad |= nonfinite_bits(v);
+__device__ __forceinline__ void accumulate_nonfinite(float2& acc, double2 v) {
+  const float2 hi = make_float2(__int_as_float(__double2hiint(v.x)), __int_as_float(__double2hiint(v.y)));
+  acc = fma2(hi, make_float2(0.f, 0.f), acc);
+}
+template <int R>
+__device__ __forceinline__ bool nonfinite_exact(const float2 (&)[R]) {
+  return true;  // the fp32 filter is exact
+}
+template <int R>
+__device__ __forceinline__ bool nonfinite_exact(const double2 (&v)[R]) {
+  uint32_t bad = 0;
+#pragma unroll
+  for (int m = 0; m < R; ++m) bad |= nonfinite_bits(v[m]);
+  return bad != 0;
 }
 
 __host__ __device__ constexpr int high_pow2(int q) {
@@ -197,74 +226,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
   }
 }
 
-// LOADER 0: each thread loads its R elements straight into registers (LDG).
-// LOADER 1: one thread issues a single bulk TMA copy of the CTA's SEQ
-//           consecutive sequences (one contiguous byte range) into shared
-//           memory, the CTA waits on an mbarrier, and pass 0 gathers from
-//           shared memory -- no per-thread global loads at all.
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0>
-__global__ void __launch_bounds__((N / R) * SEQ)
-stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
-                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+// The radix passes of one Stockham sequence, shared by both kernels below.
+// On entry v[m] = x[j + m*G] (pass-0 inputs, already validated); the
+// exchange region `smq` (per-sequence for LAYOUT 1, CTA-wide for LAYOUT 2
+// with `sbase` = s*N) is free; on exit the outputs are stored to `dst_row`
+// (nullptr: sequence past the batch, nothing stored) and the region has been
+// read for the last time by this thread.
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
+__device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __restrict__ smq, int sbase, int j,
+                                                int s, cx_t<T>* __restrict__ dst_row,
+                                                const cx_t<T>* __restrict__ tw) {
   using C = cx_t<T>;
   using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
   constexpr int NP = num_passes(N, R);
-  constexpr int SN = S::size(N);  // smem elements per sequence
-  static_assert(G >= 1 && (N % R) == 0, "geometry");
-  static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
-
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* sm = reinterpret_cast<C*>(smem_raw);
-
-  const int tid = threadIdx.x;
-  const int s = tid / G;
-  const int j = tid - s * G;
-  const long long seq = (long long)blockIdx.x * SEQ + s;
-  const bool valid = seq < batch;
-  // LAYOUT 1 keeps each sequence in its own padded region; LAYOUT 0 swizzles
-  // the CTA-wide element index (sequences are N apart, N a multiple of 16).
-  const int sbase = LAYOUT == 1 ? 0 : s * N;
-  C* smq = LAYOUT == 1 ? sm + s * SN : sm;
-
-  C v[R];
-  if constexpr (LOADER == 1) {
-    __shared__ __align__(8) unsigned long long bar;
-    const long long seq0 = (long long)blockIdx.x * SEQ;
-    const long long nseq = batch - seq0 < SEQ ? batch - seq0 : SEQ;
-    if (tid == 0) {
-      mbar_init(&bar, 1);
-      const uint32_t bytes = uint32_t(nseq * N * int(sizeof(C)));
-      mbar_expect_tx(&bar, bytes);
-      bulk_g2s(sm, in + seq0 * N, bytes, &bar);
-    }
-    __syncthreads();  // barrier initialised before anyone polls it
-    mbar_wait(&bar, 0);
-    if (valid) {
-#pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = sm[s * N + j + m * G];  // linear staging, conflict-free
-    } else {
-#pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
-    }
-    __syncthreads();  // staging fully read before the exchange layout reuses it
-  } else {
-    if (valid) {
-      const C* src = in + seq * N + j;
-#pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
-    } else {
-#pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = C{T(0), T(0)};
-    }
-  }
-  if (nonfinite != nullptr) {
-    float2 acc = make_float2(0.f, 0.f);
-    uint32_t bad = 0;
-#pragma unroll
-    for (int m = 0; m < R; ++m) accumulate_nonfinite<T>(acc, bad, v[m]);
-    if (bad || acc.x != acc.x || acc.y != acc.y) atomicOr(nonfinite, 1);
-  }
   if constexpr (INV) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
@@ -302,8 +277,8 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
     }
     if constexpr (p == NP - 1) {
       // last pass: output index b + q*L == j + m*G -> coalesced store
-      if (valid) {
-        C* dst = out + seq * N + j;
+      if (dst_row != nullptr) {
+        C* dst = dst_row + j;
 #pragma unroll
         for (int m = 0; m < R; ++m) {
           C y = v[m];
@@ -326,6 +301,158 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
       seq_sync<G, SEQ>(s);
     }
   });
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void check_nonfinite(const cx_t<T> (&v)[R], int* nonfinite) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int m = 0; m < R; ++m) accumulate_nonfinite(acc, v[m]);
+  if ((acc.x != acc.x || acc.y != acc.y) && nonfinite_exact(v)) atomicOr(nonfinite, 1);
+}
+
+// LOADER 0: each thread loads its R elements straight into registers (LDG).
+// LOADER 1: one thread issues a single bulk TMA copy of the CTA's SEQ
+//           consecutive sequences (one contiguous byte range) into shared
+//           memory, the CTA waits on an mbarrier, and pass 0 gathers from
+//           shared memory -- no per-thread global loads at all.
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0>
+__global__ void __launch_bounds__((N / R) * SEQ)
+stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
+                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  using S = Smem<T, LAYOUT, R>;
+  constexpr int G = N / R;
+  constexpr int SN = S::size(N);  // smem elements per sequence
+  static_assert(G >= 1 && (N % R) == 0, "geometry");
+  static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int s = tid / G;
+  const int j = tid - s * G;
+  const long long seq = (long long)blockIdx.x * SEQ + s;
+  const bool valid = seq < batch;
+
+  C v[R];
+  if constexpr (LOADER == 1) {
+    __shared__ __align__(8) unsigned long long bar;
+    const long long seq0 = (long long)blockIdx.x * SEQ;
+    const long long nseq = batch - seq0 < SEQ ? batch - seq0 : SEQ;
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      const uint32_t bytes = uint32_t(nseq * N * int(sizeof(C)));
+      mbar_expect_tx(&bar, bytes);
+      bulk_g2s(sm, in + seq0 * N, bytes, &bar);
+    }
+    __syncthreads();  // barrier initialised before anyone polls it
+    mbar_wait(&bar, 0);
+    // rows past the batch read stale staging; they are never stored and are
+    // excluded from the non-finite check below
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = sm[s * N + j + m * G];  // linear staging, conflict-free
+    __syncthreads();  // staging fully read before the exchange layout reuses it
+  } else {
+    // rows past the batch (last CTA only) re-read the last row instead of
+    // branching around the loads (saves a zero-fill of R registers); they are
+    // computed but never stored
+    const C* src = in + (valid ? seq : batch - 1) * N + j;
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+  }
+  if (nonfinite != nullptr && valid) check_nonfinite<T, R>(v, nonfinite);
+  // LAYOUT 1 keeps each sequence in its own padded region; LAYOUT 2 swizzles
+  // the CTA-wide element index (sequences are N apart, N a multiple of R).
+  stockham_passes<T, N, R, SEQ, INV, LAYOUT, TWP>(v, LAYOUT == 1 ? sm + s * SN : sm, LAYOUT == 1 ? 0 : s * N, j,
+                                                  s, valid ? out + seq * N : nullptr, tw);
+}
+
+// Persistent, pipelined variant: a grid of (SMs x resident CTAs) walks the
+// batch in tiles of SEQ sequences (tile t, t + grid, ...).  Each CTA owns
+// STAGES shared-memory buffers; one thread keeps STAGES - 1 bulk TMA copies
+// (cp.async.bulk + mbarrier complete_tx) of the CTA's next tiles in flight
+// while every thread computes the current one, whose staging buffer then
+// doubles as the exchange buffer of its passes.  Loads stay in flight through
+// the compute phases, independent of how fast the SMs clock.
+// Measured (profiles/r01_pipe_vs_resident.txt): 5.2-6.3 TB/s against
+// 6.9 TB/s for the resident-CTA kernel above, burst and sustained alike.  The
+// in-flight tiles must live in shared memory, so at equal on-chip bytes the
+// pipeline runs 2-3 CTAs (8-12 warps) per SM where the LDG kernel runs 4-7
+// (16-28 warps) with its in-flight lines in L1 -- the extra 100+ KB of L1 is
+// what the resident design buys, and the pipeline's compute becomes
+// latency-bound.  Kept as a tested variant, not a default.
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
+__global__ void __launch_bounds__((N / R) * SEQ)
+stockham_pipe_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
+                     const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  using S = Smem<T, LAYOUT, R>;
+  constexpr int G = N / R;
+  constexpr int SN = S::size(N);
+  constexpr int BUF = SEQ * SN;  // elements per stage buffer (>= SEQ*N linear staging)
+  static_assert(STAGES >= 2 && STAGES <= 8, "stages");
+  static_assert(G >= 1 && (N % R) == 0, "geometry");
+  static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  __shared__ __align__(8) unsigned long long full[STAGES];
+
+  const int tid = threadIdx.x;
+  const int s = tid / G;
+  const int j = tid - s * G;
+  const long long ntiles = (batch + SEQ - 1) / SEQ;
+  const long long step = gridDim.x;
+
+  auto issue = [&](long long tile, int b) {  // one thread
+    const long long seq0 = tile * SEQ;
+    const long long nseq = batch - seq0 < SEQ ? batch - seq0 : SEQ;
+    const uint32_t bytes = uint32_t(nseq * N * int(sizeof(C)));
+    mbar_expect_tx(&full[b], bytes);
+    bulk_g2s(sm + b * BUF, in + seq0 * N, bytes, &full[b]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < STAGES; ++b) mbar_init(&full[b], 1);
+#pragma unroll
+    for (int b = 0; b < STAGES - 1; ++b) {
+      const long long tile = blockIdx.x + b * step;
+      if (tile < ntiles) issue(tile, b);
+    }
+  }
+  __syncthreads();  // barriers initialised before anyone polls them
+
+  int b = 0;
+  uint32_t phase = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += step) {
+    // refill the buffer freed by the previous tile: STAGES - 1 loads stay in
+    // flight while this one is computed
+    if (tid == 0) {
+      const long long ahead = tile + (STAGES - 1) * step;
+      if (ahead < ntiles) issue(ahead, b == 0 ? STAGES - 1 : b - 1);
+    }
+    C* buf = sm + b * BUF;
+    const long long seq = tile * SEQ + s;
+    const bool valid = seq < batch;
+    mbar_wait(&full[b], phase);
+    C v[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = buf[s * N + j + m * G];  // linear staging, conflict-free
+    if (nonfinite != nullptr && valid) check_nonfinite<T, R>(v, nonfinite);
+    __syncthreads();  // staging fully read before the exchange layout reuses it
+    stockham_passes<T, N, R, SEQ, INV, LAYOUT, TWP>(v, LAYOUT == 1 ? buf + s * SN : buf, LAYOUT == 1 ? 0 : s * N,
+                                                    j, s, valid ? out + seq * N : nullptr, tw);
+    // every generic-proxy access to `buf` is done before the async proxy
+    // (the refill issued at the top of the next iteration) overwrites it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (++b == STAGES) {
+      b = 0;
+      phase ^= 1;
+    }
+  }
 }
 
 // -------------------------------------------------------------- tile kernel

@@ -3,7 +3,7 @@
 Re-derives, per 128-byte phase, for every compiled kernel variant (queried from the library with
 sfft_variant_info), the addresses each warp instruction touches in shared
 memory -- the Stockham scatter/gather of csrc/sfft_kernels.cuh with its XOR
-swizzle, and the tile kernel's 16-byte chunk staging -- and counts
+row swizzle or padding, and the tile kernel's 16-byte chunk staging -- and counts
 bank-conflict wavefronts with the 32 x 4-byte bank model.  The default
 variant of every (precision, N) must be conflict-free; ncu's
 l1tex__data_bank_conflicts_pipe_lsu_mem_shared counters confirm it on the GPU.
@@ -16,10 +16,10 @@ from paper_2203_09384_b200 import _native
 ALL_N = [2**p for p in range(1, 12)]
 
 
-def swz_elem(e: int, esize: int) -> int:
-    if esize == 8:
-        return e ^ (((e >> 4) ^ (e >> 8)) & 15)
-    return e ^ (((e >> 3) ^ (e >> 6)) & 7)
+def swz_row(e: int, r: int, esize: int) -> int:
+    """LAYOUT 2: e ^ ((e / R) & (W - 1)), W = complex elements per 128-byte row."""
+    w = 128 // esize
+    return e ^ ((e // r) & (w - 1))
 
 
 def swz_chunk(c: int) -> int:
@@ -56,7 +56,8 @@ def stockham_instructions(info, esize):
     def addr(s, e):
         if layout == 1:
             return s * region + e + e // r
-        return swz_elem(s * n + e, esize)
+        assert layout == 2
+        return swz_row(s * n + e, r, esize)
 
     lanes = [(lane // g, lane % g) if g < 32 else (0, lane) for lane in range(32)]
     out = []
@@ -127,6 +128,7 @@ def test_every_variant_bounded(n, prec):
 
 
 def test_swizzles_are_bijections():
-    for esize in (8, 16):
-        assert sorted(swz_elem(e, esize) for e in range(4096)) == list(range(4096))
+    for esize, rs in ((8, (16, 32)), (16, (8, 16, 32))):
+        for r in rs:
+            assert sorted(swz_row(e, r, esize) for e in range(4096)) == list(range(4096))
     assert sorted(swz_chunk(c) for c in range(4096)) == list(range(4096))

@@ -16,13 +16,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2203_09384_b200 as sf  # noqa: E402
 
 quick = "--quick" in sys.argv
+# --loader L: only the variants with that input path (e.g. 2 = persistent TMA pipeline)
+only_loader = int(sys.argv[sys.argv.index("--loader") + 1]) if "--loader" in sys.argv else None
 lib = sf._native.lib()
 count = 0
 for prec in ("single", "double"):
     for p in range(1, 12):
         n = 2**p
         nvar = lib.sfft_num_variants(n, 0 if prec == "single" else 1)
-        for v in range(1 if quick else nvar):
+        for v in range(1 if quick and only_loader is None else nvar):
+            if only_loader is not None and sf._native.variant_info(n, 0 if prec == "single" else 1, v)["loader"] != only_loader:
+                continue
             for d in ("forward", "inverse"):
                 batch = 37 if quick else 261
                 x = torch.from_numpy(sf.generate_batch(batch, n, seed=1, precision=prec)).cuda()

@@ -7,6 +7,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import torch
 
@@ -40,8 +41,11 @@ def main():
     ap.add_argument("--all-variants", action="store_true")
     ap.add_argument("--variant", type=int, default=None)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--cool", type=float, default=0.0,
+                    help="idle seconds before each timing (lets power/clocks recover)")
     args = ap.parse_args()
-    peak = 6549.8
+    peaks = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    peak = json.load(open(peaks))["hbm_gbs"] if os.path.exists(peaks) else 6549.8
     dev = torch.device("cuda:0")
     rows_out = []
     lib = sf._native.lib()
@@ -58,6 +62,9 @@ def main():
             vlist = range(nvar) if args.all_variants else [args.variant or 0]
             for v in vlist:
                 plan = sf.make_plan(n, args.dir, precision=prec, variant=v)
+                if args.cool > 0:
+                    torch.cuda.synchronize()
+                    time.sleep(args.cool)
                 us = time_plan(plan, x, y, rows, args.iters, args.warmup)
                 gbs = 2 * rows * n * esz / us / 1e3
                 gflops = 5 * n * max(1, n.bit_length() - 1) * rows / us / 1e3
