@@ -264,12 +264,12 @@ const std::vector<Variant>& variants(int precision, int log2n) {
            stockham_variant<double, 256, 16, 8, 2>()},
           {stockham_variant<double, 512, 16, 4, 2, 1>(), stockham_variant<double, 512, 16, 2, 2>(),
            stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 2>()},
-          {stockham_variant<double, 1024, 16, 2, 2, 1>(), stockham_variant<double, 1024, 16, 1, 2, 1>(),
+          {stockham_variant<double, 1024, 16, 1, 2, 1>(), stockham_variant<double, 1024, 16, 2, 2, 1>(),
            stockham_variant<double, 1024, 16, 1, 2>(), stockham_variant<double, 1024, 8, 1, 2>(),
            stockham_variant<double, 1024, 16, 2, 2, 1, 1>()},
-          {stockham_variant<double, 2048, 16, 1, 2, 1>(), stockham_variant<double, 2048, 16, 1, 2>(),
+          {stockham_variant<double, 2048, 16, 1, 2, 1, 1>(), stockham_variant<double, 2048, 16, 1, 2>(),
            stockham_variant<double, 2048, 8, 1, 2, 1>(), stockham_variant<double, 2048, 16, 1, 1>(),
-           stockham_variant<double, 2048, 16, 1, 2, 1, 1>(), pipe_variant<double, 2048, 16, 1, 2, 1, 3>()},
+           stockham_variant<double, 2048, 16, 1, 2, 1>(), pipe_variant<double, 2048, 16, 1, 2, 1, 3>()},
       },
   };
   return table[precision][log2n];

@@ -42,6 +42,7 @@ METRICS = [
 ]
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+US = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}  # -> us
 
 
 def raw(rep):
@@ -71,12 +72,12 @@ def main():
         lines.append(f"  dram bytes read+write per launch = {rd + wr:.0f}")
         summary = {"kernel": rec["Kernel Name"][0], "dram_bytes_per_launch": rd + wr,
                    "dram_read": rd, "dram_write": wr, "source": os.path.basename(args.rep),
-                   "duration_us_ncu": float(rec["gpu__time_duration.sum"][0]) / (1e3 if rec["gpu__time_duration.sum"][1] == "nsecond" else 1)}
+                   "duration_us_ncu": float(rec["gpu__time_duration.sum"][0]) * US.get(rec["gpu__time_duration.sum"][1], 1.0)}
     if args.launches:
         rows = [r for r in csv.DictReader(l for l in open(args.launches) if not l.startswith("=="))]
         agg = collections.defaultdict(list)
         for r in rows:
-            agg[r["Kernel Name"]].append(float(r["Metric Value"]))
+            agg[r["Kernel Name"]].append(float(r["Metric Value"]) * 1e3 * US.get(r.get("Metric Unit", "nsecond"), 1e-3))
         tot = sum(sum(v) for v in agg.values())
         lines.append("launch list (ncu gpu__time_duration.sum, cold-cache, serialised):")
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
