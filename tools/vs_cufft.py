@@ -1,0 +1,139 @@
+"""The paper's comparison on B200: our kernels vs the vendor library (cuFFT).
+
+    python tools/vs_cufft.py [--json out.json] [--bytes 1073741824]
+
+The paper benchmarks SYCL-FFT against cuFFT (PAPER.md:289-310, 380-386,
+417-418).  This tool does the same for the B200 kernels: for every N and
+precision it times, on the same 1 GiB device-resident batch, our default
+kernel and cuFFT, interleaved round by round with CUDA events, and reports GB/s of algorithmic traffic for
+both plus the accuracy of both against the complex128 direct DFT on 64 rows.
+cuFFT is called two ways: directly (cufftPlanMany + cufftExecC2C/Z2Z through
+ctypes, out-of-place into the same output buffer -- the library's own speed)
+and through torch.fft.fft without `out=` (what a PyTorch user gets; with
+`out=` torch adds a copy and halves the rate).  cuFFT is a measurement
+reference only -- it is never on the product path.
+"""
+import argparse
+import ctypes
+import glob
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402  (test/measurement infrastructure: the exact DFT)
+import paper_2203_09384_b200 as sf  # noqa: E402
+
+
+def _cufft():
+    import torch as _t
+    cands = glob.glob(os.path.join(os.path.dirname(_t.__file__), "..", "nvidia", "cufft", "lib", "libcufft.so*"))
+    cands += ["libcufft.so.11", "/usr/local/cuda/lib64/libcufft.so"]
+    for c in cands:
+        try:
+            return ctypes.CDLL(c)
+        except OSError:
+            continue
+    raise RuntimeError("libcufft not found")
+
+
+class CufftPlan:
+    """Batched 1-D out-of-place C2C (fp32) / Z2Z (fp64) plan on the current stream."""
+
+    def __init__(self, n, rows, prec):
+        self.lib = _cufft()
+        self.h = ctypes.c_int(0)
+        dims = (ctypes.c_int * 1)(n)
+        typ = 0x29 if prec == "single" else 0x69  # CUFFT_C2C / CUFFT_Z2Z
+        rc = self.lib.cufftPlanMany(ctypes.byref(self.h), 1, dims, None, 1, n, None, 1, n, typ, int(rows))
+        if rc != 0:
+            raise RuntimeError(f"cufftPlanMany failed: {rc}")
+        self.lib.cufftSetStream(self.h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        self.exec = self.lib.cufftExecC2C if prec == "single" else self.lib.cufftExecZ2Z
+
+    def __call__(self, x, y):
+        rc = self.exec(self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), -1)  # CUFFT_FORWARD
+        if rc != 0:
+            raise RuntimeError(f"cufftExec failed: {rc}")
+
+    def __del__(self):
+        try:
+            self.lib.cufftDestroy(self.h)
+        except Exception:
+            pass
+
+
+def timed(fn, iters):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e3  # us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bytes", type=int, default=1 << 30)
+    ap.add_argument("--n", default=",".join(str(2**p) for p in range(1, 12)))
+    ap.add_argument("--prec", default="single,double")
+    ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    out = []
+    for prec in args.prec.split(","):
+        esz = 8 if prec == "single" else 16
+        cdt = torch.complex64 if prec == "single" else torch.complex128
+        for n in map(int, args.n.split(",")):
+            rows = args.bytes // (n * esz)
+            x = torch.empty((rows, n), dtype=cdt, device="cuda")
+            x.real.uniform_(-1, 1)
+            x.imag.uniform_(-1, 1)
+            y = torch.empty_like(x)
+            plan = sf.make_plan(n, "forward", precision=prec)
+            cplan = CufftPlan(n, rows, prec)
+            ours = lambda: sf.launch(plan, x, y, rows)  # noqa: E731
+            lib = lambda: cplan(x, y)  # noqa: E731
+            tfft = lambda: torch.fft.fft(x, dim=-1)  # noqa: E731
+            for f in (ours, lib, tfft, ours, lib, tfft):
+                f()
+            t_ours, t_lib, t_torch = [], [], []
+            for _ in range(args.rounds):
+                t_ours.append(timed(ours, args.iters))
+                t_lib.append(timed(lib, args.iters))
+                t_torch.append(timed(tfft, args.iters))
+            us_o, us_l, us_t = statistics.median(t_ours), statistics.median(t_lib), statistics.median(t_torch)
+            del cplan
+            gbs = lambda us: 2 * rows * n * esz / us / 1e3  # noqa: E731
+            # accuracy on a 64-row sample against the exact (complex128) DFT
+            xs = x[:64].cpu().numpy()
+            exact = oracle.direct_dft(xs, "forward")
+            sf.launch(plan, x[:64].contiguous(), y[:64], 64)
+            e_o = np.max(np.linalg.norm(y[:64].cpu().numpy() - exact, axis=1) / np.linalg.norm(exact, axis=1))
+            e_l = np.max(np.linalg.norm(torch.fft.fft(x[:64], dim=-1).cpu().numpy() - exact, axis=1)
+                         / np.linalg.norm(exact, axis=1))
+            rec = {"prec": prec, "n": n, "rows": rows, "ours_us": round(us_o, 2), "cufft_us": round(us_l, 2),
+                   "torch_fft_us": round(us_t, 2),
+                   "ours_gbs": round(gbs(us_o), 1), "cufft_gbs": round(gbs(us_l), 1),
+                   "torch_fft_gbs": round(gbs(us_t), 1),
+                   "speedup_vs_cufft": round(us_l / us_o, 3),
+                   "ours_rel_l2_vs_exact": float(e_o), "cufft_rel_l2_vs_exact": float(e_l)}
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+            del x, y
+            torch.cuda.empty_cache()
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
