@@ -382,8 +382,9 @@ def run_gpu(args, n, batch, precision, direction, workload):
         "e2e": {
             "value": round(e2e_value, 1),
             "unit": UNIT,
-            "h2d_bytes_per_step": batch * rb,
-            "d2h_bytes_per_step": batch * rb,
+            # whole job (all ranks), like `value`
+            "h2d_bytes_per_step": global_batch * rb,
+            "d2h_bytes_per_step": global_batch * rb,
             "path": "execute(plan, pinned numpy, out=pinned numpy) -> sfft_execute_host",
             "ms_per_step": round(e2e_s * 1e3, 3),
             "bound": "host link (PCIe)",
@@ -397,7 +398,10 @@ def run_gpu(args, n, batch, precision, direction, workload):
             "peak": peak,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(workload),
+            # the ncu capture is of one launch at the config's batch; a
+            # strong-scaling rank launches batch/world rows
+            "traffic": (None if ncu_traffic(workload) is None
+                        else round(ncu_traffic(workload) * batch / (global_batch if args.scaling == "strong" else batch))),
             "algorithmic_bytes_per_launch": batch * 2 * rb,
             "kernel_ms": round(kernel_ms, 4),
             "peak_source": peak_src,
