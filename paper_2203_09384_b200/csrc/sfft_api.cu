@@ -350,17 +350,17 @@ int carveout_override() {
   return v;
 }
 
-// Host pipeline shape: streams and chunk size (env SFFT_HOST_STREAMS /
-// SFFT_HOST_CHUNK_MB override the defaults, read once).
+// Host pipeline shape: device buffer slots and chunk size (env
+// SFFT_HOST_SLOTS / SFFT_HOST_CHUNK_MB override the defaults, read once).
 struct HostPipelineShape {
-  // measured on the B200 host link (profiles/r01_e2e_sweep.jsonl): 32 MiB
-  // chunks reach ~97% of the concurrent H2D+D2H rate; streams >= 2 suffice
-  int streams = 3;
+  // measured on the B200 host link (profiles/r01_e2e_sweep.jsonl,
+  // r01_e2e_link.jsonl): 32 MiB chunks, 3 slots in flight
+  int slots = 3;
   int64_t chunk_bytes = int64_t(32) << 20;
   HostPipelineShape() {
-    if (const char* e = std::getenv("SFFT_HOST_STREAMS")) {
+    if (const char* e = std::getenv("SFFT_HOST_SLOTS")) {
       const int v = std::atoi(e);
-      if (v >= 1 && v <= kMaxHostStreams) streams = v;
+      if (v >= 2 && v <= kMaxHostStreams) slots = v;
     }
     if (const char* e = std::getenv("SFFT_HOST_CHUNK_MB")) {
       const long v = std::atol(e);
@@ -423,12 +423,17 @@ struct sfft_plan {
   const Variant* v = nullptr;
   void* d_tw = nullptr;
   std::vector<unsigned char> host_base;  // base table in plan precision
-  // host-buffer pipeline state (lazily created, guarded by host_mu)
+  // host-buffer pipeline state (lazily created, guarded by host_mu):
+  // one stream per engine (H2D copies, kernels, D2H copies) and `nslots`
+  // device chunk buffers cycled through them, ordered by per-slot events
   std::mutex host_mu;
   bool host_ready = false;
   int64_t host_chunk_rows = 0;
-  int nstreams = 0;
-  cudaStream_t streams[kMaxHostStreams] = {};
+  int nslots = 0;
+  cudaStream_t st_h2d = nullptr, st_kernel = nullptr, st_d2h = nullptr;
+  cudaEvent_t ev_h2d[kMaxHostStreams] = {};  // slot's H2D done (kernel may read d_in)
+  cudaEvent_t ev_k[kMaxHostStreams] = {};    // slot's kernel done (d_in free, D2H may read d_out)
+  cudaEvent_t ev_d2h[kMaxHostStreams] = {};  // slot's D2H done (d_out and host staging free)
   void* d_in[kMaxHostStreams] = {};
   void* d_out[kMaxHostStreams] = {};
   int32_t* h_flag = nullptr;  // pinned + mapped: kernels OR into it, host reads it
@@ -439,7 +444,6 @@ struct sfft_plan {
   unsigned char* h_chunk_in[kMaxHostStreams] = {};
   unsigned char* h_chunk_out[kMaxHostStreams] = {};
   int64_t h_chunk_bytes = 0;
-  cudaEvent_t slot_done[kMaxHostStreams] = {};
 };
 
 extern "C" {
@@ -560,17 +564,18 @@ int sfft_plan_destroy(sfft_plan_t p) {
     DeviceGuard guard(p->device);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->host_ready) {
-      for (int i = 0; i < p->nstreams; ++i) {
-        cudaStreamSynchronize(p->streams[i]);
-        cudaFree(p->d_in[i]);
-        cudaFree(p->d_out[i]);
-        cudaStreamDestroy(p->streams[i]);
+      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
       }
       cudaFreeHost(p->h_flag);
       for (int i = 0; i < kMaxHostStreams; ++i) {
+        cudaFree(p->d_in[i]);
+        cudaFree(p->d_out[i]);
         if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
         if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
-        if (p->slot_done[i]) cudaEventDestroy(p->slot_done[i]);
+        for (cudaEvent_t ev : {p->ev_h2d[i], p->ev_k[i], p->ev_d2h[i]})
+          if (ev) cudaEventDestroy(ev);
       }
     }
     if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -704,9 +709,12 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   const int64_t row_bytes = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
   cudaError_t e = cudaSuccess;
   if (!p->host_ready) {
-    p->nstreams = host_shape().streams;
-    for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i)
-      e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
+    p->nslots = host_shape().slots;
+    for (cudaStream_t* st : {&p->st_h2d, &p->st_kernel, &p->st_d2h})
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+    for (int i = 0; i < p->nslots && e == cudaSuccess; ++i)
+      for (cudaEvent_t* ev : {&p->ev_h2d[i], &p->ev_k[i], &p->ev_d2h[i]})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e == cudaSuccess)
       e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_flag), sizeof(int32_t) * kMaxHostStreams,
                         cudaHostAllocMapped | cudaHostAllocPortable);
@@ -721,14 +729,14 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   const int64_t max_chunk_rows = chunk_bytes / row_bytes > 0 ? chunk_bytes / row_bytes : 1;
   const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
   if (want_rows > p->host_chunk_rows) {
-    for (int i = 0; i < p->nstreams; ++i) {
-      cudaStreamSynchronize(p->streams[i]);
+    for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
+    for (int i = 0; i < p->nslots; ++i) {
       cudaFree(p->d_in[i]);
       cudaFree(p->d_out[i]);
       p->d_in[i] = p->d_out[i] = nullptr;
     }
     p->host_chunk_rows = 0;
-    for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i) {
+    for (int i = 0; i < p->nslots && e == cudaSuccess; ++i) {
       e = cudaMalloc(&p->d_in[i], want_rows * row_bytes);
       if (e == cudaSuccess) e = cudaMalloc(&p->d_out[i], want_rows * row_bytes);
     }
@@ -754,7 +762,7 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
       src = p->h_stage;
       dst = p->h_stage + kSmallCallBytes;
     }
-    cudaStream_t st = p->streams[0];
+    cudaStream_t st = p->st_h2d;
     e = cudaMemcpyAsync(p->d_in[0], src, size_t(total), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = p->v->launch[p->direction](p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dst, p->d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
@@ -762,35 +770,43 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
     if (!pinned) std::memcpy(h_out, dst, size_t(total));
   } else {
+    // Three engines, one stream each -- H2D copies, kernels, D2H copies --
+    // with chunk k in device slot k % S.  Per slot:
+    //   H2D(k)    waits kernel(k-S)  (d_in free)
+    //   kernel(k) waits H2D(k) and D2H(k-S)  (d_out free)
+    //   D2H(k)    waits kernel(k)
+    // so each copy engine sees an uninterrupted queue in its own direction.
+    // Measured (tools/e2e_link_probe.py, profiles/r01_e2e_link.jsonl): 97-99 %
+    // of two free-running full-size concurrent copies on the same box; the
+    // link, not the pipeline, is the bound.  (Geometric ramp-in/ramp-out
+    // chunk sizes against fill/drain measured no gain.)
     const unsigned char* src = static_cast<const unsigned char*>(h_in);
     unsigned char* dst = static_cast<unsigned char*>(h_out);
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
+    const int S = p->nslots;
     const int64_t stage_bytes = p->host_chunk_rows * row_bytes;
     if (!pinned && p->h_chunk_bytes < stage_bytes) {
-      for (int i = 0; i < p->nstreams; ++i) {
-        cudaStreamSynchronize(p->streams[i]);
+      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
+      for (int i = 0; i < S; ++i) {
         if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
         if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
         p->h_chunk_in[i] = p->h_chunk_out[i] = nullptr;
       }
       p->h_chunk_bytes = 0;
-      for (int i = 0; i < p->nstreams && e == cudaSuccess; ++i) {
+      for (int i = 0; i < S && e == cudaSuccess; ++i) {
         e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_in[i]), stage_bytes, cudaHostAllocPortable);
         if (e == cudaSuccess)
           e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_out[i]), stage_bytes, cudaHostAllocPortable);
-        if (e == cudaSuccess && p->slot_done[i] == nullptr)
-          e = cudaEventCreateWithFlags(&p->slot_done[i], cudaEventDisableTiming);
       }
       if (e != cudaSuccess) return cuda_fail(e, "pinned chunk staging allocation");
       p->h_chunk_bytes = stage_bytes;
     }
     auto& pool = sfft_host::CopyPool::instance();
-    // chunk bookkeeping for the staged (pageable) path: slot -> (row, rows)
+    // staged (pageable) path: which rows each slot's host staging holds
     int64_t slot_row[kMaxHostStreams] = {}, slot_rows[kMaxHostStreams] = {};
-    for (int i = 0; i < kMaxHostStreams; ++i) slot_rows[i] = 0;
     auto drain_slot = [&](int s) -> cudaError_t {
       if (slot_rows[s] == 0) return cudaSuccess;
-      const cudaError_t err = cudaEventSynchronize(p->slot_done[s]);
+      const cudaError_t err = cudaEventSynchronize(p->ev_d2h[s]);
       if (err != cudaSuccess) return err;
       pool.memcpy(dst + slot_row[s] * row_bytes, p->h_chunk_out[s], size_t(slot_rows[s] * row_bytes));
       slot_rows[s] = 0;
@@ -798,42 +814,49 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     };
     int chunk = 0;
     for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
-      const int s = chunk % p->nstreams;
+      const int s = chunk % S;
+      const bool reuse = chunk >= S;  // the slot's previous chunk is in flight
       const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
       const size_t bytes = size_t(rows * row_bytes);
-      cudaStream_t st = p->streams[s];
       const void* h2d_src = src + row * row_bytes;
       void* d2h_dst = dst + row * row_bytes;
       if (!pinned) {
-        // the slot's previous chunk must have left the staging buffers
+        // the slot's previous chunk must have left the host staging (its D2H
+        // done implies its H2D done)
         e = drain_slot(s);
         if (e != cudaSuccess) return cuda_fail(e, "staging drain");
         pool.memcpy(p->h_chunk_in[s], src + row * row_bytes, bytes);
         h2d_src = p->h_chunk_in[s];
         d2h_dst = p->h_chunk_out[s];
       }
-      e = cudaMemcpyAsync(p->d_in[s], h2d_src, bytes, cudaMemcpyHostToDevice, st);
+      if (reuse) e = cudaStreamWaitEvent(p->st_h2d, p->ev_k[s], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_in[s], h2d_src, bytes, cudaMemcpyHostToDevice, p->st_h2d);
+      if (e == cudaSuccess) e = cudaEventRecord(p->ev_h2d[s], p->st_h2d);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, st);
+      e = cudaStreamWaitEvent(p->st_kernel, p->ev_h2d[s], 0);
+      if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(p->st_kernel, p->ev_d2h[s], 0);
+      if (e == cudaSuccess)
+        e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel);
+      if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[s], p->st_kernel);
       if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-      e = cudaMemcpyAsync(d2h_dst, p->d_out[s], bytes, cudaMemcpyDeviceToHost, st);
+      e = cudaStreamWaitEvent(p->st_d2h, p->ev_k[s], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(d2h_dst, p->d_out[s], bytes, cudaMemcpyDeviceToHost, p->st_d2h);
+      if (e == cudaSuccess) e = cudaEventRecord(p->ev_d2h[s], p->st_d2h);
       if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
       if (!pinned) {
-        e = cudaEventRecord(p->slot_done[s], st);
-        if (e != cudaSuccess) return cuda_fail(e, "event record");
         slot_row[s] = row;
         slot_rows[s] = rows;
       }
     }
     if (!pinned) {
       // drain in chunk order (oldest first)
-      for (int k = 0; k < p->nstreams; ++k) {
-        e = drain_slot((chunk + k) % p->nstreams);
+      for (int k = 0; k < S; ++k) {
+        e = drain_slot((chunk + k) % S);
         if (e != cudaSuccess) return cuda_fail(e, "staging drain");
       }
     }
-    for (int i = 0; i < p->nstreams; ++i) {
-      e = cudaStreamSynchronize(p->streams[i]);
+    for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) {
+      e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return cuda_fail(e, "stream sync");
     }
   }

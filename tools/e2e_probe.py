@@ -1,6 +1,6 @@
 """Time execute() on pinned host buffers (the bench e2e leg) for one host-pipeline shape.
 
-    SFFT_HOST_STREAMS=4 SFFT_HOST_CHUNK_MB=16 python tools/e2e_probe.py [n] [batch]
+    SFFT_HOST_SLOTS=4 SFFT_HOST_CHUNK_MB=16 python tools/e2e_probe.py [n] [batch]
 """
 import json
 import os
@@ -26,5 +26,5 @@ reps = 10
 for _ in range(reps):
     sf.execute(plan, a, out=b)
 dt = (time.perf_counter() - t) / reps
-print(json.dumps({"streams": os.environ.get("SFFT_HOST_STREAMS"), "chunk_mb": os.environ.get("SFFT_HOST_CHUNK_MB"),
+print(json.dumps({"slots": os.environ.get("SFFT_HOST_SLOTS"), "chunk_mb": os.environ.get("SFFT_HOST_CHUNK_MB"),
                   "ms": round(dt * 1e3, 3), "gbs_each_way": round(batch * n * 8 / dt / 1e9, 1)}))
