@@ -76,7 +76,8 @@ __host__ __device__ constexpr int twiddle_table_len(int n, int r) {
 //           map(base + c) = map'(base, (c / R) mod W) + c, and for an
 //           R-aligned base and c < R, map(base + c) = base + (c ^ term) --
 //           every access of a pass is one of <= W precomputed registers plus
-//           an immediate (no per-access shift/xor chain as in LAYOUT 0) and
+//           an immediate (no per-access shift/xor chain, unlike a plain XOR
+//           swizzle of e with higher bits of e) and
 //           no padding (16-byte accesses stay 128-byte aligned per phase,
 //           which LAYOUT 1 breaks).
 // tests/test_bank_model.py replays every access of every variant per phase.
