@@ -127,7 +127,7 @@ class _NativePlans:
             lib.sfft_plan_destroy(ctypes.c_void_p(h))
         handles.clear()
 
-    def handle(self, device: int) -> ctypes.c_void_p:
+    def handle(self, device: int) -> int:
         h = self.handles.get(device)
         if h is None:
             with self.lock:
@@ -142,7 +142,7 @@ class _NativePlans:
                     )
                     h = out.value
                     self.handles[device] = h
-        return ctypes.c_void_p(h)
+        return h  # the C-ABI argtypes (c_void_p) take the address as an int
 
 
 @dataclass(frozen=True)
@@ -202,7 +202,7 @@ class FftPlan:
     def dtype(self):
         return self.precision.dtype
 
-    def native_handle(self, device: int) -> ctypes.c_void_p:
+    def native_handle(self, device: int) -> int:
         """The per-device ``sfft_plan_t`` (created and uploaded on first call)."""
         return self._handles.handle(int(device))
 

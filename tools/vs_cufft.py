@@ -1,6 +1,7 @@
 """The paper's comparison on B200: our kernels vs the vendor library (cuFFT).
 
     python tools/vs_cufft.py [--json out.json] [--bytes 1073741824]
+    python tools/vs_cufft.py --latency [--json out.json]     # one transform per call
 
 The paper benchmarks SYCL-FFT against cuFFT (PAPER.md:289-310, 380-386,
 417-418).  This tool does the same for the B200 kernels: for every N and
@@ -79,8 +80,48 @@ def timed(fn, iters):
     return e0.elapsed_time(e1) / iters * 1e3  # us
 
 
+def latency(args):
+    """Paper Table 2 on B200: one transform per call, 1000 timed calls after a
+    warm-up, host wall clock per call (launch + stream sync), mean and min
+    ("optimal").  Both arms are driven from Python
+    through ctypes, so the host overhead is the same kind on both sides."""
+    import time
+
+    out = []
+    stream = torch.cuda.current_stream()
+    for n in [2**p for p in range(3, 12)]:
+        x = torch.empty((1, n), dtype=torch.complex64, device="cuda")
+        x.real.uniform_(-1, 1)
+        x.imag.uniform_(-1, 1)
+        y = torch.empty_like(x)
+        plan = sf.make_plan(n, "forward")
+        cplan = CufftPlan(n, 1, "single")
+        arms = {
+            "ours_launch_sync": lambda: (sf.launch(plan, x, y, 1, stream=stream), stream.synchronize()),
+            "cufft_exec_sync": lambda: (cplan(x, y), stream.synchronize()),
+            "ours_execute": lambda: sf.execute(plan, x),
+        }
+        rec = {"n": n}
+        for name, fn in arms.items():
+            for _ in range(50):
+                fn()
+            ts = []
+            for _ in range(args.latency_calls):
+                t0 = time.perf_counter_ns()
+                fn()
+                ts.append((time.perf_counter_ns() - t0) / 1e3)
+            rec[name + "_mean_us"] = round(statistics.mean(ts), 2)
+            rec[name + "_min_us"] = round(min(ts), 2)
+        del cplan
+        out.append(rec)
+        print(json.dumps(rec), flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--latency", action="store_true", help="single-transform latency protocol instead")
+    ap.add_argument("--latency-calls", type=int, default=1000)
     ap.add_argument("--bytes", type=int, default=1 << 30)
     ap.add_argument("--n", default=",".join(str(2**p) for p in range(1, 12)))
     ap.add_argument("--prec", default="single,double")
@@ -88,6 +129,12 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
+    if args.latency:
+        out = latency(args)
+        if args.json:
+            with open(args.json, "w") as f:
+                json.dump(out, f, indent=1)
+        return
     out = []
     for prec in args.prec.split(","):
         esz = 8 if prec == "single" else 16
