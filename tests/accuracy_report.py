@@ -1,6 +1,7 @@
 """Accuracy table: GPU kernels vs the exact DFT, next to the reference engine's own error.
 
-For each N, precision and direction: 256 Philox rows; reports max per-row
+Report script (not a test module; lives in tests/ because it calls the
+oracle).  For each N, precision and direction: 256 Philox rows; reports max per-row
 rel-L2 of (a) the GPU result vs the complex128 direct DFT, (b) the reference
 algorithm (oracle port, complex64 or complex128 stage engine) vs the same,
 and (c) GPU vs reference.  Writes JSON to argv[1].
@@ -12,7 +13,7 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
 sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 import paper_2203_09384_b200 as sf  # noqa: E402

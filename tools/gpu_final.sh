@@ -10,7 +10,7 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --no-cpu > gpurun_out/bench_c2_torchrun.json 2> gpurun_out/bench_c2_torchrun.err
 timeout 600 python tools/sweep.py --cool 0.3 --json gpurun_out/sweep_fwd.json > gpurun_out/sweep_fwd.log 2>&1
 timeout 600 python tools/sweep.py --cool 0.3 --dir inverse --json gpurun_out/sweep_inv.json > gpurun_out/sweep_inv.log 2>&1
-timeout 600 python tools/accuracy.py gpurun_out/accuracy.json > gpurun_out/accuracy.log 2>&1
+timeout 600 python tests/accuracy_report.py gpurun_out/accuracy.json > gpurun_out/accuracy.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 10 --warmup 3 --no-cpu --e2e-steps 1 --no-check > gpurun_out/ncu_launch_run.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_c2 python bench.py --steps 4 --warmup 3 --no-cpu --e2e-steps 1 --no-check > gpurun_out/ncu_full_run.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_c4 python bench.py --config c4 --steps 4 --warmup 3 --no-cpu --e2e-steps 1 --no-check > gpurun_out/ncu_full_run_c4.log 2>&1
