@@ -274,7 +274,6 @@ def run_gpu(args, n, batch, precision, direction, workload):
         return sf.sharding.max_over_ranks(v, device=dev)
 
     cdt = torch.complex64 if precision == "single" else torch.complex128
-    ndt = np.complex64 if precision == "single" else np.complex128
     rb = row_bytes(n, precision)
     global_batch = batch * world
     if args.scaling == "strong":  # fixed total work, contiguous row shards
