@@ -142,3 +142,32 @@ def test_large_full_size_properties(cuda):
     ex = torch.sum(torch.abs(x.to(torch.complex128)) ** 2, dim=1)
     ey = torch.sum(torch.abs(y.to(torch.complex128)) ** 2, dim=1) / n
     assert ((ex - ey).abs() / ex).max().item() <= 1e-5
+
+
+@pytest.mark.parametrize("n,prec", [(1024, "single"), (2048, "double"), (8, "single")])
+def test_launch_is_cuda_graph_capturable(cuda, n, prec):
+    """`launch` only enqueues work on the given stream, so a chain of
+    transforms (forward then inverse here) can be captured once into a CUDA
+    graph and replayed -- the launch-bound way to run many small batches."""
+    x = torch.from_numpy(sf.generate_batch(33, n, seed=3, precision=prec)).to(cuda)
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    fwd = sf.make_plan(n, "forward", precision=prec)
+    inv = sf.make_plan(n, "inverse", precision=prec)
+    s = torch.cuda.Stream(cuda)
+    with torch.cuda.stream(s):  # native plans + kernel attributes exist before capture
+        sf.launch(fwd, x, y, 33, stream=s)
+        sf.launch(inv, y, z, 33, stream=s)
+    s.synchronize()
+    want_y, want_z = y.clone(), z.clone()
+    y.zero_()
+    z.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sf.launch(fwd, x, y, 33, stream=s)
+        sf.launch(inv, y, z, 33, stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want_y) and torch.equal(z, want_z)
+    tol = (1e-5 if prec == "single" else 1e-13) * np.log2(n)
+    assert rel_l2(z.cpu().numpy(), x.cpu().numpy()) <= 2 * tol
