@@ -143,14 +143,42 @@ def test_nonfinite_input_raises(cuda, prec, n):
 @pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("n", [8, 256, 2048])
 def test_host_path_matches_device_path(cuda, prec, n):
-    # > 16 MiB so sfft_execute_host pipelines several chunks over 3 streams
-    rows = (40 << 20) // (n * (8 if prec == "single" else 16))
+    # 40 MiB + a ragged tail: 2 chunks of the 32 MiB pipeline
+    rows = (40 << 20) // (n * (8 if prec == "single" else 16)) + 3
     x = sf.generate_batch(rows, n, seed=5, precision=prec)
     plan = sf.make_plan(n, precision=prec)
     host = sf.execute(plan, x)
     dev = run(plan, x, cuda)
     assert isinstance(host, np.ndarray) and host.dtype == dtype_of(prec)
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("memory", ["pageable", "pinned", "pinned_in_pageable_out"])
+def test_host_pipeline_reuses_slots(cuda, memory):
+    """> 3 x 32 MiB so every device slot (and, for pageable memory, every
+    pinned staging slot) is reused: exercises the per-slot event ordering of
+    sfft_execute_host and the drain order of the staged path."""
+    n, prec = 1024, "single"
+    rows = (7 * (32 << 20) + (5 << 20)) // (n * 8) + 1  # 7.2 chunks, ragged tail
+    x = sf.generate_batch(rows, n, seed=11, precision=prec)
+    plan = sf.make_plan(n, precision=prec)
+    want = run(plan, x[: rows // 3], cuda), run(plan, x[rows // 3:], cuda)
+    if memory == "pageable":
+        xin, out = x, np.empty_like(x)
+    else:
+        xin = torch.from_numpy(x).pin_memory().numpy()
+        out = (torch.empty(x.shape, dtype=torch.complex64, pin_memory=True).numpy()
+               if memory == "pinned" else np.empty_like(x))
+    for _ in range(2):  # second call reuses the events of the first
+        got = sf.execute(plan, xin, out=out)
+        assert got is out
+        assert np.array_equal(got[: rows // 3], want[0]) and np.array_equal(got[rows // 3:], want[1])
+    # a NaN in the last chunk still raises, and the plan stays usable
+    bad = x.copy()
+    bad[-1, 5] = np.nan
+    with pytest.raises(sf.DomainError):
+        sf.execute(plan, bad)
+    assert np.array_equal(sf.execute(plan, x)[:4], want[0][:4])
 
 
 def test_input_dtypes_and_shapes(cuda):
