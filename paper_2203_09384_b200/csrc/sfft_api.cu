@@ -36,8 +36,9 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(SFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// pdl: launch with programmatic stream serialization (see launch_pdl)
 using LaunchFn = cudaError_t (*)(const void* in, void* out, const void* tw, long long batch,
-                                 int* flag, cudaStream_t st);
+                                 int* flag, cudaStream_t st, bool pdl);
 using PrepareFn = cudaError_t (*)(int carveout);
 
 struct Variant {
@@ -65,17 +66,45 @@ constexpr int stockham_smem() {
   return SEQ * sfft::Smem<T, LAYOUT, R>::size(N) * int(sizeof(sfft::cx_t<T>));
 }
 
+// SFFT_PDL=0 disables programmatic dependent launch (A/B and debugging).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SFFT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+// (the kernels call griddepcontrol.wait before any global access).
+// Used for launches on the caller's stream; the host pipeline, whose kernels
+// follow cross-stream event waits, launches with pdl = false.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), long long grid, int threads, int smem, cudaStream_t st,
+                       Args... args) {
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
 cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
   constexpr int threads = (N / R) * SEQ;
   constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   const long long grid = (batch + SEQ - 1) / SEQ;
-  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER><<<dim3(unsigned(grid)), threads, smem, st>>>(
-      static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
-  return cudaGetLastError();
+  return launch_pdl(pdl, sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>, grid, threads, smem, st,
+                    static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
 }
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
 cudaError_t prepare_stockham(int carveout) {
@@ -110,7 +139,7 @@ int persistent_grid(K kernel, int threads, int smem) {
 
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
 cudaError_t launch_stockham_pipe(const void* in, void* out, const void* tw, long long batch, int* flag,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
   constexpr int threads = (N / R) * SEQ;
   constexpr int smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
@@ -119,9 +148,8 @@ cudaError_t launch_stockham_pipe(const void* in, void* out, const void* tw, long
   const int full = persistent_grid(k, threads, smem);
   if (full <= 0) return cudaErrorInvalidConfiguration;
   const long long grid = tiles < full ? tiles : full;
-  k<<<dim3(unsigned(grid)), threads, smem, st>>>(static_cast<const C*>(in), static_cast<C*>(out),
-                                                 static_cast<const C*>(tw), batch, flag);
-  return cudaGetLastError();
+  return launch_pdl(pdl, k, grid, threads, smem, st, static_cast<const C*>(in), static_cast<C*>(out),
+                    static_cast<const C*>(tw), batch, flag);
 }
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
 cudaError_t prepare_stockham_pipe(int carveout) {
@@ -139,15 +167,13 @@ constexpr int tile_smem(int n, int spt, int warps) {
 
 template <typename T, int N, int SPT, int W, bool INV>
 cudaError_t launch_tile(const void* in, void* out, const void*, long long batch, int* flag,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
   constexpr int smem = tile_smem<T>(N, SPT, W);
   constexpr long long per_cta = 32LL * SPT * W;
   const long long grid = (batch + per_cta - 1) / per_cta;
-  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  sfft::tile_kernel<T, N, SPT, W, INV><<<dim3(unsigned(grid)), 32 * W, smem, st>>>(
-      static_cast<const C*>(in), static_cast<C*>(out), batch, flag);
-  return cudaGetLastError();
+  return launch_pdl(pdl, sfft::tile_kernel<T, N, SPT, W, INV>, grid, 32 * W, smem, st, static_cast<const C*>(in),
+                    static_cast<C*>(out), batch, flag);
 }
 template <typename T, int N, int SPT, int W, bool INV>
 cudaError_t prepare_tile(int carveout) {
@@ -658,7 +684,7 @@ int sfft_execute(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, vo
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   const cudaError_t e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch,
                                                    reinterpret_cast<int*>(d_nonfinite),
-                                                   static_cast<cudaStream_t>(stream));
+                                                   static_cast<cudaStream_t>(stream), true);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SFFT_OK;
 }
@@ -684,7 +710,7 @@ int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batc
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
     if (e != cudaSuccess) return cuda_fail(e, "event record");
   }
-  e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch, t_sync.d_flag, st);
+  e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch, t_sync.d_flag, st, true);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   if (kernel_ms) {
     e = cudaEventRecord(ev[1], st);
@@ -764,7 +790,8 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     }
     cudaStream_t st = p->st_h2d;
     e = cudaMemcpyAsync(p->d_in[0], src, size_t(total), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = p->v->launch[p->direction](p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st);
+    if (e == cudaSuccess)
+      e = p->v->launch[p->direction](p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st, false);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dst, p->d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
@@ -836,7 +863,8 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
       e = cudaStreamWaitEvent(p->st_kernel, p->ev_h2d[s], 0);
       if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(p->st_kernel, p->ev_d2h[s], 0);
       if (e == cudaSuccess)
-        e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel);
+        e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel,
+                                       false);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[s], p->st_kernel);
       if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
       e = cudaStreamWaitEvent(p->st_d2h, p->ev_k[s], 0);

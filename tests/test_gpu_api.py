@@ -171,3 +171,22 @@ def test_launch_is_cuda_graph_capturable(cuda, n, prec):
     assert torch.equal(y, want_y) and torch.equal(z, want_z)
     tol = (1e-5 if prec == "single" else 1e-13) * np.log2(n)
     assert rel_l2(z.cpu().numpy(), x.cpu().numpy()) <= 2 * tol
+
+
+@pytest.mark.parametrize("n,prec", [(1024, "single"), (2048, "double"), (16, "single"), (8, "double")])
+def test_back_to_back_launch_chain_stays_ordered(cuda, n, prec):
+    """Launches on one stream use programmatic dependent launch: kernel k+1 is
+    scheduled while kernel k drains and waits (griddepcontrol.wait) before
+    touching memory.  A long in-place forward/inverse chain on one buffer --
+    every kernel reading what the previous one wrote -- must round-trip."""
+    rows = (64 << 20) // (n * (8 if prec == "single" else 16))
+    x0 = torch.from_numpy(sf.generate_batch(rows, n, seed=9, precision=prec)).to(cuda)
+    buf = x0.clone()
+    fwd = sf.make_plan(n, "forward", precision=prec)
+    inv = sf.make_plan(n, "inverse", precision=prec)
+    for _ in range(10):
+        sf.launch(fwd, buf, buf, rows)
+        sf.launch(inv, buf, buf, rows)
+    torch.cuda.synchronize()
+    tol = (1e-5 if prec == "single" else 1e-13) * np.log2(n)
+    assert row_rel_l2(buf.cpu().numpy(), x0.cpu().numpy()).max() <= 20 * tol
