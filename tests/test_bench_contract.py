@@ -1,0 +1,67 @@
+"""bench.py's JSON-line contract (the driver parses these lines).
+
+CPU: the reference arm on a tiny config, and its rank != 0 behaviour.
+GPU: the device arm on a small config, every key the contract names.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BENCH = os.path.join(ROOT, "bench.py")
+
+
+def run_bench(args, env_extra=None, timeout=600):
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    proc = subprocess.run([sys.executable, BENCH, *args], capture_output=True, text=True, env=env,
+                          timeout=timeout, cwd=ROOT)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    lines = [ln for ln in proc.stdout.splitlines() if ln.strip()]
+    return lines
+
+
+def test_reference_arm_line():
+    lines = run_bench(["--impl", "reference", "--n", "64", "--batch", "512", "--steps", "1", "--warmup", "3"])
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] == "port"
+    assert "workload" in d["config"]
+
+
+def test_reference_arm_other_ranks_print_nothing():
+    lines = run_bench(["--impl", "reference", "--n", "8", "--batch", "64", "--steps", "1", "--warmup", "3"],
+                      {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert lines == []
+
+
+def test_warmup_below_three_is_rejected():
+    proc = subprocess.run([sys.executable, BENCH, "--impl", "reference", "--warmup", "2"], capture_output=True,
+                          text=True, cwd=ROOT)
+    assert proc.returncode != 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line(cuda):
+    lines = run_bench(["--n", "256", "--batch", "65536", "--steps", "5", "--warmup", "3", "--no-cpu",
+                       "--e2e-steps", "1"])
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 5 and d["scaling"] == "weak"
+    e2e = d["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == 65536 * 256 * 8 == e2e["d2h_bytes_per_step"]
+    roof = d["roofline"]
+    assert roof["bound"] == "hbm" and roof["unit"] == "GB/s" and roof["peak"] > 0
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-3
+    assert d["gpu_launches"] == 5
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["parity_rel_l2_max_first64_vs_numpy_c128"] < 1e-5 * 8
