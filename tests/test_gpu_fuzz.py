@@ -55,3 +55,24 @@ def test_random_shapes_match_oracle(cuda, c):
     tol = tolerance(n, prec)
     assert row_rel_l2(got, exact).max() <= tol
     assert row_rel_l2(got, want).max() <= 2 * tol
+
+
+@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(p=st.integers(1, 11), prec=st.sampled_from(["single", "double"]),
+       direction=st.sampled_from(["forward", "inverse"]), batch=st.integers(0, 3000),
+       pinned=st.booleans(), seed=st.integers(0, 2**31 - 1))
+def test_host_path_equals_device_path(cuda, p, prec, direction, batch, pinned, seed):
+    """numpy in -> numpy out (sfft_execute_host: small-call bounce path or the
+    chunked pipeline, pageable or pinned) is bit-identical to the device path,
+    for 1-D (batch 0 means a single (N,) signal) and 2-D inputs."""
+    n = 2**p
+    x = sf.generate_batch(max(batch, 1), n, seed=seed, precision=prec)
+    if batch == 0:
+        x = x[0]
+    if pinned:
+        x = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+    plan = sf.make_plan(n, direction, precision=prec)
+    host = sf.execute(plan, x)
+    dev = sf.execute(plan, torch.from_numpy(np.ascontiguousarray(x)).to(cuda)).cpu().numpy()
+    assert host.shape == x.shape and host.dtype == x.dtype
+    assert np.array_equal(host, dev)
