@@ -76,6 +76,7 @@ typedef struct sfft_plan_info {
                                   2: persistent CTAs, pipelined bulk TMA copies */
   int32_t smem_carveout;       /* preferred shared-memory carveout, % of max (-1: driver default) */
   int32_t pipeline_stages;     /* loader 2: shared-memory stage buffers per CTA (else 0) */
+  int32_t real_input;          /* 1: SFFT_INPUT_REAL is supported (sfft_execute_ex) */
 } sfft_plan_info_t;
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -130,6 +131,24 @@ int sfft_execute(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch,
  * kernel's device time from CUDA events recorded around the launch. */
 int sfft_execute_sync(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch,
                       void* stream, float* kernel_ms);
+
+/* Input kinds of the _ex entry points.  SFFT_INPUT_REAL: `d_in` holds
+ * `batch` rows of n REAL values (float for SFFT_SINGLE, double for
+ * SFFT_DOUBLE; element-aligned) -- the C2C transform of a real signal, as
+ * the reference computes for real input (executor.py:74 casts it to
+ * complex; tests/test_executor.py:89-92).  The kernel reads the reals and
+ * zero imaginary parts in registers: half the input traffic, no widening
+ * pass.  Available when sfft_plan_info().real_input is 1 (the default
+ * Stockham kernels, n >= 64 fp32 / n >= 32 fp64); otherwise
+ * SFFT_ERR_ARGUMENT. */
+#define SFFT_INPUT_COMPLEX 0
+#define SFFT_INPUT_REAL 1
+
+/* sfft_execute / sfft_execute_sync with an input kind. */
+int sfft_execute_ex(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch, void* stream,
+                    int32_t* d_nonfinite, int32_t input_kind);
+int sfft_execute_sync_ex(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch,
+                         void* stream, float* kernel_ms, int32_t input_kind);
 
 /* Synchronous execute on host memory: chunked H2D -> kernel -> D2H pipeline
  * over several streams (pinned memory gives full PCIe/C2C bandwidth);

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libsfft.so")
 SFFT_SINGLE, SFFT_DOUBLE = 0, 1
 SFFT_FORWARD, SFFT_INVERSE = 0, 1
 SFFT_KERNEL_STOCKHAM, SFFT_KERNEL_TILE = 0, 1
+SFFT_INPUT_COMPLEX, SFFT_INPUT_REAL = 0, 1
 
 #: every symbol include/sfft.h declares (tests check the .so exports them all)
 EXPORTED_SYMBOLS = (
@@ -34,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "sfft_plan_twiddles",
     "sfft_execute",
     "sfft_execute_sync",
+    "sfft_execute_ex",
+    "sfft_execute_sync_ex",
     "sfft_execute_host",
     "sfft_permute",
     "sfft_stage",
@@ -64,6 +67,7 @@ class PlanInfo(ctypes.Structure):
         ("loader", ctypes.c_int32),
         ("smem_carveout", ctypes.c_int32),
         ("pipeline_stages", ctypes.c_int32),
+        ("real_input", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -90,6 +94,8 @@ def _bind(lib):
         "sfft_variant_info": ([i32, i32, i32, ctypes.POINTER(PlanInfo)], ctypes.c_int),
         "sfft_execute": ([p, p, p, i64, p, p], ctypes.c_int),
         "sfft_execute_sync": ([p, p, p, i64, p, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+        "sfft_execute_ex": ([p, p, p, i64, p, p, i32], ctypes.c_int),
+        "sfft_execute_sync_ex": ([p, p, p, i64, p, ctypes.POINTER(ctypes.c_float), i32], ctypes.c_int),
         "sfft_execute_host": ([p, p, p, i64], ctypes.c_int),
         "sfft_permute": ([i32, i32, p, p, p, i64, p], ctypes.c_int),
         "sfft_stage": ([i32, i32, i32, i32, i32, p, p, p, i64, p], ctypes.c_int),

@@ -4,12 +4,14 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sfft.h"
@@ -58,6 +60,10 @@ struct Variant {
   int tw_len;      // per-pass twiddle elements
   LaunchFn launch[2];    // [direction]
   PrepareFn prepare[2];  // [direction]
+  // real-valued input rows (imaginary parts zero), default variants only;
+  // always the per-thread (LDG) loader with the LDG carveout
+  LaunchFn launch_real[2];
+  PrepareFn prepare_real[2];
 };
 
 // ---------------------------------------------------------------- launchers
@@ -96,19 +102,20 @@ cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), long long grid, int t
   return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
 }
 
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
 cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
                             cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
   constexpr int threads = (N / R) * SEQ;
   constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   const long long grid = (batch + SEQ - 1) / SEQ;
-  return launch_pdl(pdl, sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>, grid, threads, smem, st,
-                    static_cast<const C*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
+  return launch_pdl(pdl, sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>, grid, threads, smem,
+                    st, static_cast<const In*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
 }
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
 cudaError_t prepare_stockham(int carveout) {
-  const auto k = sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER>;
+  const auto k = sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        stockham_smem<T, N, R, SEQ, LAYOUT>());
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
@@ -184,7 +191,7 @@ cudaError_t prepare_tile(int carveout) {
   return e;
 }
 
-template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0>
+template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0, bool REAL = false>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
@@ -210,6 +217,12 @@ Variant stockham_variant() {
   v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, 0, true>;
+    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, 0, true>;
+    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, 0, true>;
+    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, 0, true>;
+  }
   return v;
 }
 
@@ -260,19 +273,19 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<float, 8, 4, 4>(), tile_variant<float, 8, 2, 4>()},
           {tile_variant<float, 16, 2, 4>(), tile_variant<float, 16, 1, 8>()},
           {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32, 1>()},
-          {stockham_variant<float, 64, 8, 16, 1>(), stockham_variant<float, 64, 16, 32, 1>()},
-          {stockham_variant<float, 128, 16, 16, 2>(), stockham_variant<float, 128, 16, 16, 1>(),
+          {stockham_variant<float, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<float, 64, 16, 32, 1>()},
+          {stockham_variant<float, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<float, 128, 16, 16, 1>(),
            stockham_variant<float, 128, 8, 8, 1>()},
-          {stockham_variant<float, 256, 16, 8, 1>(), stockham_variant<float, 256, 16, 8, 2>(),
+          {stockham_variant<float, 256, 16, 8, 1, 0, 0, true>(), stockham_variant<float, 256, 16, 8, 2>(),
            stockham_variant<float, 256, 16, 8, 1, 1>(), stockham_variant<float, 256, 16, 8, 1, 0, 1>()},
-          {stockham_variant<float, 512, 16, 4, 1, 1>(), stockham_variant<float, 512, 16, 2, 1>(),
+          {stockham_variant<float, 512, 16, 4, 1, 1, 0, true>(), stockham_variant<float, 512, 16, 2, 1>(),
            stockham_variant<float, 512, 16, 4, 1>()},
-          {stockham_variant<float, 1024, 32, 2, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1, 1, 1>(),
+          {stockham_variant<float, 1024, 32, 2, 1, 1, 0, true>(), stockham_variant<float, 1024, 16, 1, 1, 1, 1>(),
            stockham_variant<float, 1024, 16, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1>(),
            stockham_variant<float, 1024, 32, 4, 1>(), stockham_variant<float, 1024, 16, 2, 1>(),
            stockham_variant<float, 1024, 16, 2, 1, 1, 1>(), stockham_variant<float, 1024, 32, 4, 1, 1>(),
            pipe_variant<float, 1024, 16, 2, 1, 1, 3>()},
-          {stockham_variant<float, 2048, 16, 1, 1, 1>(), stockham_variant<float, 2048, 16, 1, 1>(),
+          {stockham_variant<float, 2048, 16, 1, 1, 1, 0, true>(), stockham_variant<float, 2048, 16, 1, 1>(),
            stockham_variant<float, 2048, 16, 1, 2>(), stockham_variant<float, 2048, 32, 1, 1>(),
            stockham_variant<float, 2048, 16, 1, 1, 1, 1>(), stockham_variant<float, 2048, 32, 1, 1, 1>(),
            stockham_variant<float, 2048, 32, 2, 1, 1>()},
@@ -283,17 +296,17 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<double, 4, 2, 4>(), tile_variant<double, 4, 1, 8>()},
           {tile_variant<double, 8, 1, 4>(), tile_variant<double, 8, 2, 4>()},
           {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64, 2>()},
-          {stockham_variant<double, 32, 8, 32, 1>(), stockham_variant<double, 32, 8, 32, 2>()},
-          {stockham_variant<double, 64, 8, 16, 1>(), stockham_variant<double, 64, 8, 16, 2>()},
-          {stockham_variant<double, 128, 16, 16, 2>(), stockham_variant<double, 128, 8, 8, 1>()},
-          {stockham_variant<double, 256, 16, 8, 2, 1>(), stockham_variant<double, 256, 8, 4, 1>(),
+          {stockham_variant<double, 32, 8, 32, 1, 0, 0, true>(), stockham_variant<double, 32, 8, 32, 2>()},
+          {stockham_variant<double, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<double, 64, 8, 16, 2>()},
+          {stockham_variant<double, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<double, 128, 8, 8, 1>()},
+          {stockham_variant<double, 256, 16, 8, 2, 1, 0, true>(), stockham_variant<double, 256, 8, 4, 1>(),
            stockham_variant<double, 256, 16, 8, 2>()},
-          {stockham_variant<double, 512, 16, 4, 2, 1>(), stockham_variant<double, 512, 16, 2, 2>(),
+          {stockham_variant<double, 512, 16, 4, 2, 1, 0, true>(), stockham_variant<double, 512, 16, 2, 2>(),
            stockham_variant<double, 512, 8, 2, 1>(), stockham_variant<double, 512, 16, 4, 2>()},
-          {stockham_variant<double, 1024, 16, 1, 2, 1>(), stockham_variant<double, 1024, 16, 2, 2, 1>(),
+          {stockham_variant<double, 1024, 16, 1, 2, 1, 0, true>(), stockham_variant<double, 1024, 16, 2, 2, 1>(),
            stockham_variant<double, 1024, 16, 1, 2>(), stockham_variant<double, 1024, 8, 1, 2>(),
            stockham_variant<double, 1024, 16, 2, 2, 1, 1>()},
-          {stockham_variant<double, 2048, 16, 1, 2, 1, 1>(), stockham_variant<double, 2048, 16, 1, 2>(),
+          {stockham_variant<double, 2048, 16, 1, 2, 1, 1, true>(), stockham_variant<double, 2048, 16, 1, 2>(),
            stockham_variant<double, 2048, 8, 1, 2, 1>(), stockham_variant<double, 2048, 16, 1, 1>(),
            stockham_variant<double, 2048, 16, 1, 2, 1>(), pipe_variant<double, 2048, 16, 1, 2, 1, 3>()},
       },
@@ -570,6 +583,8 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
     }
   }
   e = p->v->prepare[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
+  if (e == cudaSuccess && p->v->prepare_real[direction])  // LDG loader: the LDG carveout rule
+    e = p->v->prepare_real[direction](carveout_override() >= -1 ? carveout_override() : 50);
   if (e != cudaSuccess) {
     cudaFree(p->d_tw);
     delete p;
@@ -632,6 +647,7 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   info->loader = p->v->loader;
   info->smem_carveout = carveout_override() >= -1 ? carveout_override() : p->v->carveout;
   info->pipeline_stages = p->v->stages;
+  info->real_input = p->v->launch_real[0] != nullptr;
   return SFFT_OK;
 }
 
@@ -661,6 +677,7 @@ int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_i
   info->loader = v.loader;
   info->smem_carveout = v.carveout;
   info->pipeline_stages = v.stages;
+  info->real_input = v.launch_real[0] != nullptr;
   return SFFT_OK;
 }
 
@@ -672,32 +689,62 @@ int sfft_plan_twiddles(sfft_plan_t p, void* host_out, int64_t capacity) {
   return SFFT_OK;
 }
 
-int sfft_execute(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
-                 int32_t* d_nonfinite) {
+namespace {
+// the kernel for (plan, input kind), or nullptr with the error recorded
+LaunchFn pick_launch(sfft_plan_t p, int32_t input_kind, const void* d_in, const void* d_out, int* rc) {
+  *rc = SFFT_OK;
+  if (input_kind != SFFT_INPUT_COMPLEX && input_kind != SFFT_INPUT_REAL) {
+    *rc = fail(SFFT_ERR_ARGUMENT, "input_kind must be SFFT_INPUT_COMPLEX or SFFT_INPUT_REAL");
+    return nullptr;
+  }
+  const uintptr_t in_align = input_kind == SFFT_INPUT_REAL ? (p->precision == SFFT_SINGLE ? 4u : 8u) : 16u;
+  if ((reinterpret_cast<uintptr_t>(d_in) % in_align) | (reinterpret_cast<uintptr_t>(d_out) & 15u)) {
+    *rc = fail(SFFT_ERR_ARGUMENT, input_kind == SFFT_INPUT_REAL
+                                      ? "real input must be element-aligned and output 16-byte aligned"
+                                      : "data pointers must be 16-byte aligned");
+    return nullptr;
+  }
+  if (input_kind == SFFT_INPUT_COMPLEX) return p->v->launch[p->direction];
+  if (p->v->launch_real[p->direction] == nullptr) {
+    *rc = fail(SFFT_ERR_ARGUMENT, "this plan's kernel has no real-input path (see sfft_plan_info.real_input)");
+    return nullptr;
+  }
+  return p->v->launch_real[p->direction];
+}
+}  // namespace
+
+int sfft_execute_ex(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                    int32_t* d_nonfinite, int32_t input_kind) {
   if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
   if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
   if (batch == 0) return SFFT_OK;
   if (d_in == nullptr || d_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
-  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)
-    return fail(SFFT_ERR_ARGUMENT, "data pointers must be 16-byte aligned");
+  int rc = SFFT_OK;
+  const LaunchFn launch = pick_launch(p, input_kind, d_in, d_out, &rc);
+  if (launch == nullptr) return rc;
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
-  const cudaError_t e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch,
-                                                   reinterpret_cast<int*>(d_nonfinite),
-                                                   static_cast<cudaStream_t>(stream), true);
+  const cudaError_t e = launch(d_in, d_out, p->d_tw, batch, reinterpret_cast<int*>(d_nonfinite),
+                               static_cast<cudaStream_t>(stream), true);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SFFT_OK;
 }
 
-int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
-                      float* kernel_ms) {
+int sfft_execute(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                 int32_t* d_nonfinite) {
+  return sfft_execute_ex(p, d_in, d_out, batch, stream, d_nonfinite, SFFT_INPUT_COMPLEX);
+}
+
+int sfft_execute_sync_ex(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                         float* kernel_ms, int32_t input_kind) {
   if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
   if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
   if (kernel_ms) *kernel_ms = 0.f;
   if (batch == 0) return SFFT_OK;
   if (d_in == nullptr || d_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
-  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)
-    return fail(SFFT_ERR_ARGUMENT, "data pointers must be 16-byte aligned");
+  int rc = SFFT_OK;
+  const LaunchFn launch = pick_launch(p, input_kind, d_in, d_out, &rc);
+  if (launch == nullptr) return rc;
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   cudaError_t e = t_sync.flag();
@@ -710,7 +757,7 @@ int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batc
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
     if (e != cudaSuccess) return cuda_fail(e, "event record");
   }
-  e = p->v->launch[p->direction](d_in, d_out, p->d_tw, batch, t_sync.d_flag, st, true);
+  e = launch(d_in, d_out, p->d_tw, batch, t_sync.d_flag, st, true);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   if (kernel_ms) {
     e = cudaEventRecord(ev[1], st);
@@ -722,6 +769,11 @@ int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batc
   if (*reinterpret_cast<volatile int32_t*>(t_sync.h_flag))
     return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
   return SFFT_OK;
+}
+
+int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch, void* stream,
+                      float* kernel_ms) {
+  return sfft_execute_sync_ex(p, d_in, d_out, batch, stream, kernel_ms, SFFT_INPUT_COMPLEX);
 }
 
 int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch) {

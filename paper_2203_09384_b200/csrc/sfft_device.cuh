@@ -77,6 +77,13 @@ template <typename C> __device__ __forceinline__ C csub(C a, C b) { return C{a.x
 template <typename C> __device__ __forceinline__ C cmul(C a, C w) {
   return C{a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
 }
+// fp64: the FMA structure is spelled out (__fma_rn / __dmul_rn) instead of
+// left to contraction, so every kernel instantiation rounds identically --
+// e.g. the real-input loader (imaginary parts known zero in pass 0) stays
+// bit-identical to widening the input to complex first.
+template <> __device__ __forceinline__ double2 cmul<double2>(double2 a, double2 w) {
+  return double2{__fma_rn(a.x, w.x, -__dmul_rn(a.y, w.y)), __fma_rn(a.x, w.y, __dmul_rn(a.y, w.x))};
+}
 
 // CUDA's sm_100 float2 intrinsics (crt/sm_100_rt.h) keep (re, im) in one
 // register pair; hand-packing through a u64 (shift/or) instead costs a MOV /
@@ -130,14 +137,16 @@ __device__ __forceinline__ C twiddle_const(C a) {
       return fma2(make_float2(-a.y, a.x), make_float2(s, s), mul2(a, make_float2(c, c)));  // immediates
     }
   } else {
+    // __dmul_rn: the products must not be contracted into the butterfly
+    // adds that consume them (see cmul<double2>)
     if constexpr (8 * j == L) {  // (1 - i)/sqrt2
-      return C{(a.x + a.y) * h, (a.y - a.x) * h};
+      return C{__dmul_rn(a.x + a.y, h), __dmul_rn(a.y - a.x, h)};
     } else if constexpr (8 * j == 3 * L) {  // (-1 - i)/sqrt2
-      return C{(a.y - a.x) * h, -(a.x + a.y) * h};
+      return C{__dmul_rn(a.y - a.x, h), -__dmul_rn(a.x + a.y, h)};
     } else if constexpr (8 * j == 5 * L) {  // (-1 + i)/sqrt2
-      return C{-(a.x + a.y) * h, (a.x - a.y) * h};
+      return C{-__dmul_rn(a.x + a.y, h), __dmul_rn(a.x - a.y, h)};
     } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
-      return C{(a.x - a.y) * h, (a.x + a.y) * h};
+      return C{__dmul_rn(a.x - a.y, h), __dmul_rn(a.x + a.y, h)};
     } else {
       constexpr int j32 = j * (32 / L);
       constexpr T c = T(cos32(j32));
@@ -177,6 +186,8 @@ __device__ __forceinline__ void dft_regs(C (&v)[R]) {
 
 // ----------------------------------------------------- global memory streams
 // Streaming (evict-first) accesses: every element is read once and written once.
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }

@@ -330,10 +330,14 @@ __device__ __forceinline__ void pdl_enter() {
 //           consecutive sequences (one contiguous byte range) into shared
 //           memory, the CTA waits on an mbarrier, and pass 0 gathers from
 //           shared memory -- no per-thread global loads at all.
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0>
+// RIN: the input rows are real (N values of T each, imaginary parts zero) --
+//      the C2C transform of a real signal reads 4 (8) bytes per element
+//      instead of 8 (16) and needs no separate widening pass (LOADER 0 only).
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0, bool RIN = false>
 __global__ void __launch_bounds__((N / R) * SEQ)
-stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
+stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
                 const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  static_assert(!RIN || LOADER == 0, "real input uses the per-thread loader");
   using C = cx_t<T>;
   using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
@@ -373,9 +377,14 @@ stockham_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
     // rows past the batch (last CTA only) re-read the last row instead of
     // branching around the loads (saves a zero-fill of R registers); they are
     // computed but never stored
-    const C* src = in + (valid ? seq : batch - 1) * N + j;
+    const auto* src = in + (valid ? seq : batch - 1) * N + j;
+    if constexpr (RIN) {
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+      for (int m = 0; m < R; ++m) v[m] = C{ld_stream(src + m * G), T(0)};
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
+    }
   }
   if (nonfinite != nullptr && valid) check_nonfinite<T, R>(v, nonfinite);
   // LAYOUT 1 keeps each sequence in its own padded region; LAYOUT 2 swizzles

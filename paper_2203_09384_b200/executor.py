@@ -139,14 +139,23 @@ def _execute_host(plan: FftPlan, signal, out=None):
 
 # ----------------------------------------------------------------- torch path
 def _prepare_device(plan: FftPlan, x):
+    """(input tensor for the kernel, rows, input kind).
+
+    Real input (executor.py:74 casts it to complex; test_executor.py:89-92)
+    goes to the kernel as real rows when its loader supports that: it reads
+    half the bytes and zeroes the imaginary parts in registers, instead of a
+    widening pass to complex first."""
     rows = _check_shape(plan, tuple(x.shape))
     if x.dtype == torch.bool:  # numpy kind "b" is rejected too (executor.py:70-71)
         raise DomainError(f"signal has non-numeric dtype {x.dtype}")
-    want = torch.complex64 if plan.dtype == np.complex64 else torch.complex128
-    xc = x.to(want).contiguous()
+    single = plan.dtype == np.complex64
+    if not x.is_complex() and plan.supports_real_input(x.get_device()):
+        xr = x.to(torch.float32 if single else torch.float64).contiguous()
+        return xr, rows, _native.SFFT_INPUT_REAL
+    xc = x.to(torch.complex64 if single else torch.complex128).contiguous()
     if xc.data_ptr() % 16:
         xc = xc.clone()
-    return xc, rows
+    return xc, rows, _native.SFFT_INPUT_COMPLEX
 
 
 def launch(plan: FftPlan, x_in, x_out, rows: int, *, stream=None, flag=None) -> None:
@@ -158,27 +167,30 @@ def launch(plan: FftPlan, x_in, x_out, rows: int, *, stream=None, flag=None) -> 
     """
     dev = x_in.get_device()
     raw = _raw_stream(dev) if stream is None else stream.cuda_stream
+    kind = _native.SFFT_INPUT_COMPLEX if x_in.is_complex() else _native.SFFT_INPUT_REAL
     _native.check(
-        _native.lib().sfft_execute(
+        _native.lib().sfft_execute_ex(
             plan.native_handle(dev),
             x_in.data_ptr(),
             x_out.data_ptr(),
             rows,
             raw,
             None if flag is None else flag.data_ptr(),
+            kind,
         )
     )
 
 
 def _execute_device(plan: FftPlan, x, timed: bool = False, out=None):
     t0 = time.perf_counter_ns()
-    xc, rows = _prepare_device(plan, x)
+    xc, rows, kind = _prepare_device(plan, x)
+    cdt = torch.complex64 if plan.dtype == np.complex64 else torch.complex128
     if out is None:
-        out = torch.empty_like(xc)
+        out = torch.empty(xc.shape, dtype=cdt, device=xc.device)
     elif (
         not _is_torch(out)
         or out.device != xc.device
-        or out.dtype != xc.dtype
+        or out.dtype != cdt
         or out.numel() != xc.numel()
         or not out.is_contiguous()
         or out.data_ptr() % 16
@@ -190,13 +202,14 @@ def _execute_device(plan: FftPlan, x, timed: bool = False, out=None):
     t1 = time.perf_counter_ns()
     # one C call: launch, wait, read the mapped NaN/Inf flag (DomainError)
     _native.check(
-        _native.lib().sfft_execute_sync(
+        _native.lib().sfft_execute_sync_ex(
             handle,
             xc.data_ptr(),
             out.data_ptr(),
             rows,
             _raw_stream(dev),
             ctypes.byref(kernel_ms) if timed else None,
+            kind,
         )
     )
     return out, (t1 - t0) / 1000.0, kernel_ms.value * 1000.0 if timed else 0.0

@@ -115,6 +115,7 @@ class _NativePlans:
     def __init__(self, spec):
         self.spec = spec  # (n, precision code, direction code, batch, variant)
         self.handles: dict[int, int] = {}
+        self.real_input: dict[int, bool] = {}  # device -> kernel has the real-input loader
         self.lock = threading.Lock()
         self._finalizer = weakref.finalize(self, _NativePlans._destroy, self.handles)
 
@@ -201,6 +202,14 @@ class FftPlan:
     @property
     def dtype(self):
         return self.precision.dtype
+
+    def supports_real_input(self, device: int) -> bool:
+        """Whether the kernel reads real rows directly (sfft_execute_ex, SFFT_INPUT_REAL)."""
+        cache = self._handles.real_input
+        ok = cache.get(device)
+        if ok is None:
+            ok = cache[device] = bool(self.kernel_info(device)["real_input"])
+        return ok
 
     def native_handle(self, device: int) -> int:
         """The per-device ``sfft_plan_t`` (created and uploaded on first call)."""

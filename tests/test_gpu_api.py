@@ -190,3 +190,35 @@ def test_back_to_back_launch_chain_stays_ordered(cuda, n, prec):
     torch.cuda.synchronize()
     tol = (1e-5 if prec == "single" else 1e-13) * np.log2(n)
     assert row_rel_l2(buf.cpu().numpy(), x0.cpu().numpy()).max() <= 20 * tol
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+@pytest.mark.parametrize("n", [8, 32, 64, 1024, 2048])
+def test_real_input_path(cuda, n, prec):
+    """Real rows go to the kernel as reals where its loader supports it
+    (sfft_execute_ex, SFFT_INPUT_REAL) -- bit-identical to widening to
+    complex first, as the reference does (executor.py:74,
+    tests/test_executor.py:89-92)."""
+    rdt = torch.float32 if prec == "single" else torch.float64
+    cdt = torch.complex64 if prec == "single" else torch.complex128
+    g = torch.Generator(device=cuda).manual_seed(n)
+    xr = torch.rand((777, n), generator=g, device=cuda, dtype=rdt) * 2 - 1
+    for direction in ("forward", "inverse"):
+        plan = sf.make_plan(n, direction, precision=prec)
+        got = sf.execute(plan, xr)
+        want = sf.execute(plan, xr.to(cdt))
+        assert got.dtype == cdt and torch.equal(got, want)
+        assert torch.equal(sf.execute(plan, xr[5]), want[5])  # 1-D
+        if plan.supports_real_input(cuda.index):
+            y = torch.empty((777, n), dtype=cdt, device=cuda)
+            sf.launch(plan, xr, y, 777)
+            torch.cuda.synchronize()
+            assert torch.equal(y, want)
+    # other real dtypes are cast to the plan's real type first
+    plan = sf.make_plan(n, precision=prec)
+    xi = torch.randint(-5, 5, (33, n), device=cuda, dtype=torch.int32)
+    assert torch.equal(sf.execute(plan, xi), sf.execute(plan, xi.to(cdt)))
+    bad = xr.clone()
+    bad[-1, -1] = float("inf")
+    with pytest.raises(sf.DomainError):
+        sf.execute(plan, bad)
