@@ -157,6 +157,11 @@ int sfft_execute_sync_ex(sfft_plan_t plan, const void* d_in, void* d_out, int64_
  * Returns SFFT_ERR_DOMAIN if the input held NaN/Inf (output then undefined). */
 int sfft_execute_host(sfft_plan_t plan, const void* h_in, void* h_out, int64_t batch);
 
+/* sfft_execute_host with an input kind: SFFT_INPUT_REAL moves n reals per
+ * row host->device (half the H2D bytes) and returns complex rows. */
+int sfft_execute_host_ex(sfft_plan_t plan, const void* h_in, void* h_out, int64_t batch,
+                         int32_t input_kind);
+
 /* Stage-level API (kernels.py:28-151, planner.py:62-89) on device buffers --
  * not the hot path (that is sfft_execute: all stages fused in one HBM pass),
  * but the reference's building blocks for custom stage lists.

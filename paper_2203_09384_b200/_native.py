@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "sfft_execute_ex",
     "sfft_execute_sync_ex",
     "sfft_execute_host",
+    "sfft_execute_host_ex",
     "sfft_permute",
     "sfft_stage",
     "sfft_last_error",
@@ -97,6 +98,7 @@ def _bind(lib):
         "sfft_execute_ex": ([p, p, p, i64, p, p, i32], ctypes.c_int),
         "sfft_execute_sync_ex": ([p, p, p, i64, p, ctypes.POINTER(ctypes.c_float), i32], ctypes.c_int),
         "sfft_execute_host": ([p, p, p, i64], ctypes.c_int),
+        "sfft_execute_host_ex": ([p, p, p, i64, i32], ctypes.c_int),
         "sfft_permute": ([i32, i32, p, p, p, i64, p], ctypes.c_int),
         "sfft_stage": ([i32, i32, i32, i32, i32, p, p, p, i64, p], ctypes.c_int),
         "sfft_last_error": ([], ctypes.c_char_p),

@@ -776,15 +776,23 @@ int sfft_execute_sync(sfft_plan_t p, const void* d_in, void* d_out, int64_t batc
   return sfft_execute_sync_ex(p, d_in, d_out, batch, stream, kernel_ms, SFFT_INPUT_COMPLEX);
 }
 
-int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch) {
+int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch, int32_t input_kind) {
   if (p == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL plan");
   if (batch < 0) return fail(SFFT_ERR_SHAPE, "batch must be >= 0");
   if (batch == 0) return SFFT_OK;
   if (h_in == nullptr || h_out == nullptr) return fail(SFFT_ERR_ARGUMENT, "NULL data pointer");
+  if (input_kind != SFFT_INPUT_COMPLEX && input_kind != SFFT_INPUT_REAL)
+    return fail(SFFT_ERR_ARGUMENT, "input_kind must be SFFT_INPUT_COMPLEX or SFFT_INPUT_REAL");
+  const bool real = input_kind == SFFT_INPUT_REAL;
+  const LaunchFn launch = real ? p->v->launch_real[p->direction] : p->v->launch[p->direction];
+  if (launch == nullptr)
+    return fail(SFFT_ERR_ARGUMENT, "this plan's kernel has no real-input path (see sfft_plan_info.real_input)");
   std::lock_guard<std::mutex> lock(p->host_mu);
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  // output rows are complex; real input rows carry half the bytes (H2D only)
   const int64_t row_bytes = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
+  const int64_t in_row_bytes = real ? row_bytes / 2 : row_bytes;
   cudaError_t e = cudaSuccess;
   if (!p->host_ready) {
     p->nslots = host_shape().slots;
@@ -823,6 +831,7 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
   }
   for (int i = 0; i < kMaxHostStreams; ++i) p->h_flag[i] = 0;
   const int64_t total = batch * row_bytes;
+  const int64_t total_in = batch * in_row_bytes;
 
   if (total <= kSmallCallBytes) {
     // latency path: one stream; pageable user memory goes through a pinned
@@ -836,14 +845,13 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     const void* src = h_in;
     void* dst = h_out;
     if (!pinned) {
-      std::memcpy(p->h_stage, h_in, size_t(total));
+      std::memcpy(p->h_stage, h_in, size_t(total_in));
       src = p->h_stage;
       dst = p->h_stage + kSmallCallBytes;
     }
     cudaStream_t st = p->st_h2d;
-    e = cudaMemcpyAsync(p->d_in[0], src, size_t(total), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-      e = p->v->launch[p->direction](p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st, false);
+    e = cudaMemcpyAsync(p->d_in[0], src, size_t(total_in), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch(p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st, false);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dst, p->d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
@@ -897,26 +905,26 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
       const bool reuse = chunk >= S;  // the slot's previous chunk is in flight
       const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
       const size_t bytes = size_t(rows * row_bytes);
-      const void* h2d_src = src + row * row_bytes;
+      const size_t in_bytes = size_t(rows * in_row_bytes);
+      const void* h2d_src = src + row * in_row_bytes;
       void* d2h_dst = dst + row * row_bytes;
       if (!pinned) {
         // the slot's previous chunk must have left the host staging (its D2H
         // done implies its H2D done)
         e = drain_slot(s);
         if (e != cudaSuccess) return cuda_fail(e, "staging drain");
-        pool.memcpy(p->h_chunk_in[s], src + row * row_bytes, bytes);
+        pool.memcpy(p->h_chunk_in[s], src + row * in_row_bytes, in_bytes);
         h2d_src = p->h_chunk_in[s];
         d2h_dst = p->h_chunk_out[s];
       }
       if (reuse) e = cudaStreamWaitEvent(p->st_h2d, p->ev_k[s], 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_in[s], h2d_src, bytes, cudaMemcpyHostToDevice, p->st_h2d);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_in[s], h2d_src, in_bytes, cudaMemcpyHostToDevice, p->st_h2d);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_h2d[s], p->st_h2d);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
       e = cudaStreamWaitEvent(p->st_kernel, p->ev_h2d[s], 0);
       if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(p->st_kernel, p->ev_d2h[s], 0);
       if (e == cudaSuccess)
-        e = p->v->launch[p->direction](p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel,
-                                       false);
+        e = launch(p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel, false);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[s], p->st_kernel);
       if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
       e = cudaStreamWaitEvent(p->st_d2h, p->ev_k[s], 0);
@@ -944,6 +952,10 @@ int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batc
     if (reinterpret_cast<volatile int32_t*>(p->h_flag)[i])
       return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
   return SFFT_OK;
+}
+
+int sfft_execute_host(sfft_plan_t p, const void* h_in, void* h_out, int64_t batch) {
+  return sfft_execute_host_ex(p, h_in, h_out, batch, SFFT_INPUT_COMPLEX);
 }
 
 }  // extern "C"

@@ -87,16 +87,25 @@ def _default_device(plan: FftPlan) -> int:
 
 
 # ----------------------------------------------------------------- numpy path
-def _prepare_host(plan: FftPlan, signal):
+def _prepare_host(plan: FftPlan, signal, allow_real: bool = False):
+    """(original array, contiguous input for the kernel, rows, input kind).
+
+    With ``allow_real``, real input whose plan kernel has the real loader is
+    passed as real rows of the plan's real type (half the H2D bytes);
+    otherwise it is widened to the plan dtype here, as validation.py:26 /
+    executor.py:74 do (complex128 -> complex64 for a single-precision plan).
+    """
     x = np.asarray(signal)
     rows = _check_shape(plan, x.shape)
     if x.dtype.kind not in "fciu":
         raise DomainError(f"signal has non-numeric dtype {x.dtype}")
-    # complex128 -> complex64 for a single-precision plan, as validation.py:26 does
+    if allow_real and x.dtype.kind != "c" and plan.supports_real_input(_default_device(plan)):
+        real_t = np.float32 if plan.dtype == np.complex64 else np.float64
+        return x, np.ascontiguousarray(x, dtype=real_t), rows, _native.SFFT_INPUT_REAL
     xc = np.ascontiguousarray(x, dtype=plan.dtype)
     if xc.ctypes.data % 16:
         xc = xc.copy()
-    return x, xc, rows
+    return x, xc, rows, _native.SFFT_INPUT_COMPLEX
 
 
 _HUGE_OUTPUT_BYTES = 32 << 20
@@ -121,7 +130,7 @@ def _empty_host(shape, dtype) -> np.ndarray:
 
 
 def _execute_host(plan: FftPlan, signal, out=None):
-    x, xc, rows = _prepare_host(plan, signal)
+    x, xc, rows, kind = _prepare_host(plan, signal, allow_real=True)
     if out is None:
         out = _empty_host(xc.shape, plan.dtype)
     elif (
@@ -133,7 +142,7 @@ def _execute_host(plan: FftPlan, signal, out=None):
     ):
         raise ShapeError("out must be a C-contiguous, 16-byte aligned array of the plan dtype and size")
     handle = plan.native_handle(_default_device(plan))
-    _native.check(_native.lib().sfft_execute_host(handle, xc.ctypes.data, out.ctypes.data, rows))
+    _native.check(_native.lib().sfft_execute_host_ex(handle, xc.ctypes.data, out.ctypes.data, rows, kind))
     return out
 
 
@@ -242,7 +251,7 @@ def execute_timed(plan: FftPlan, signal) -> TimedExecution:
         return TimedExecution(*_execute_device(plan, signal, timed=True))
     t0 = time.perf_counter_ns()
     host = signal.numpy() if _is_torch(signal) else signal
-    x, xc, _ = _prepare_host(plan, host)
+    x, xc, _, _ = _prepare_host(plan, host)
     dev = _default_device(plan)
     xd = torch.from_numpy(xc).to(f"cuda:{dev}")
     t_h2d = time.perf_counter_ns()

@@ -59,9 +59,9 @@ def execute_sharded(plan: FftPlan, signal, devices) -> np.ndarray:
     devices = [int(d) for d in devices]
     if not devices:
         raise ShapeError("execute_sharded needs at least one device")
-    _, xc, rows = _prepare_host(plan, signal)
+    _, xc, rows, _ = _prepare_host(plan, signal, allow_real=True)
     x2 = xc.reshape(rows, plan.length)
-    out = np.empty_like(x2)
+    out = np.empty(x2.shape, dtype=plan.dtype)
 
     def run(rank: int) -> None:
         lo, hi = shard_bounds(rows, len(devices), rank)

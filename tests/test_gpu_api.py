@@ -222,3 +222,23 @@ def test_real_input_path(cuda, n, prec):
     bad[-1, -1] = float("inf")
     with pytest.raises(sf.DomainError):
         sf.execute(plan, bad)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_real_numpy_input_host_path(cuda, prec, pinned):
+    """Real numpy rows cross the host link as reals (sfft_execute_host_ex,
+    SFFT_INPUT_REAL: half the H2D bytes) -- small-call and chunked pipeline
+    paths -- bit-identical to widening on the host first."""
+    n = 1024
+    rdt = np.float32 if prec == "single" else np.float64
+    plan = sf.make_plan(n, precision=prec)
+    for rows in (3, (48 << 20) // (n * 2 * np.dtype(rdt).itemsize) + 7):  # small call, > 1 chunk
+        x = np.random.default_rng(rows).uniform(-1, 1, (rows, n)).astype(rdt)
+        if pinned:
+            x = torch.from_numpy(x).pin_memory().numpy()
+        got = sf.execute(plan, x)
+        want = sf.execute(plan, x.astype(plan.dtype))
+        assert got.dtype == plan.dtype and got.shape == x.shape
+        assert np.array_equal(got, want)
+    assert np.array_equal(sf.execute_sharded(plan, x, [0, 0]), want)
