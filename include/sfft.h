@@ -138,9 +138,8 @@ int sfft_execute_sync(sfft_plan_t plan, const void* d_in, void* d_out, int64_t b
  * the reference computes for real input (executor.py:74 casts it to
  * complex; tests/test_executor.py:89-92).  The kernel reads the reals and
  * zero imaginary parts in registers: half the input traffic, no widening
- * pass.  Available when sfft_plan_info().real_input is 1 (the default
- * Stockham kernels, n >= 64 fp32 / n >= 32 fp64); otherwise
- * SFFT_ERR_ARGUMENT. */
+ * pass.  Available when sfft_plan_info().real_input is 1 (every default
+ * kernel variant); otherwise SFFT_ERR_ARGUMENT. */
 #define SFFT_INPUT_COMPLEX 0
 #define SFFT_INPUT_REAL 1
 

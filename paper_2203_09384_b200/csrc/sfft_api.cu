@@ -167,25 +167,26 @@ cudaError_t prepare_stockham_pipe(int carveout) {
   return e;
 }
 
-template <typename T>
-constexpr int tile_smem(int n, int spt, int warps) {
-  return n * int(sizeof(sfft::cx_t<T>)) / 16 == 1 ? 0 : warps * 32 * spt * n * int(sizeof(sfft::cx_t<T>));
+template <typename T, int N, int SPT, int W, bool RIN = false>
+constexpr int tile_smem() {
+  return W * sfft::tile_chunks<T, N, SPT, RIN>() * 16;
 }
 
-template <typename T, int N, int SPT, int W, bool INV>
+template <typename T, int N, int SPT, int W, bool INV, bool RIN = false>
 cudaError_t launch_tile(const void* in, void* out, const void*, long long batch, int* flag,
                         cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
-  constexpr int smem = tile_smem<T>(N, SPT, W);
+  using In = std::conditional_t<RIN, T, C>;
+  constexpr int smem = tile_smem<T, N, SPT, W, RIN>();
   constexpr long long per_cta = 32LL * SPT * W;
   const long long grid = (batch + per_cta - 1) / per_cta;
-  return launch_pdl(pdl, sfft::tile_kernel<T, N, SPT, W, INV>, grid, 32 * W, smem, st, static_cast<const C*>(in),
-                    static_cast<C*>(out), batch, flag);
+  return launch_pdl(pdl, sfft::tile_kernel<T, N, SPT, W, INV, RIN>, grid, 32 * W, smem, st,
+                    static_cast<const In*>(in), static_cast<C*>(out), batch, flag);
 }
-template <typename T, int N, int SPT, int W, bool INV>
+template <typename T, int N, int SPT, int W, bool INV, bool RIN = false>
 cudaError_t prepare_tile(int carveout) {
-  constexpr int smem = tile_smem<T>(N, SPT, W);
-  const auto k = sfft::tile_kernel<T, N, SPT, W, INV>;
+  constexpr int smem = tile_smem<T, N, SPT, W, RIN>();
+  const auto k = sfft::tile_kernel<T, N, SPT, W, INV, RIN>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
   return e;
@@ -241,14 +242,14 @@ Variant pipe_variant() {
   return v;
 }
 
-template <typename T, int N, int SPT, int W>
+template <typename T, int N, int SPT, int W, bool REAL = false>
 Variant tile_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_TILE;
   v.r = N;
   v.seq = 32 * SPT * W;
   v.threads = 32 * W;
-  v.smem = tile_smem<T>(N, SPT, W);
+  v.smem = tile_smem<T, N, SPT, W>();
   v.passes = 1;
   v.radices[0] = N;
   v.tw_len = 0;
@@ -257,6 +258,12 @@ Variant tile_variant() {
   v.launch[1] = &launch_tile<T, N, SPT, W, true>;
   v.prepare[0] = &prepare_tile<T, N, SPT, W, false>;
   v.prepare[1] = &prepare_tile<T, N, SPT, W, true>;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_tile<T, N, SPT, W, false, true>;
+    v.launch_real[1] = &launch_tile<T, N, SPT, W, true, true>;
+    v.prepare_real[0] = &prepare_tile<T, N, SPT, W, false, true>;
+    v.prepare_real[1] = &prepare_tile<T, N, SPT, W, true, true>;
+  }
   return v;
 }
 
@@ -268,11 +275,11 @@ const std::vector<Variant>& variants(int precision, int log2n) {
   static const std::vector<Variant> table[2][12] = {
       {
           {},
-          {tile_variant<float, 2, 8, 4>(), tile_variant<float, 2, 4, 8>()},
-          {tile_variant<float, 4, 4, 4>(), tile_variant<float, 4, 2, 8>()},
-          {tile_variant<float, 8, 4, 4>(), tile_variant<float, 8, 2, 4>()},
-          {tile_variant<float, 16, 2, 4>(), tile_variant<float, 16, 1, 8>()},
-          {tile_variant<float, 32, 1, 4>(), stockham_variant<float, 32, 8, 32, 1>()},
+          {tile_variant<float, 2, 8, 4, true>(), tile_variant<float, 2, 4, 8>()},
+          {tile_variant<float, 4, 4, 4, true>(), tile_variant<float, 4, 2, 8>()},
+          {tile_variant<float, 8, 4, 4, true>(), tile_variant<float, 8, 2, 4>()},
+          {tile_variant<float, 16, 2, 4, true>(), tile_variant<float, 16, 1, 8>()},
+          {tile_variant<float, 32, 1, 4, true>(), stockham_variant<float, 32, 8, 32, 1>()},
           {stockham_variant<float, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<float, 64, 16, 32, 1>()},
           {stockham_variant<float, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<float, 128, 16, 16, 1>(),
            stockham_variant<float, 128, 8, 8, 1>()},
@@ -292,10 +299,10 @@ const std::vector<Variant>& variants(int precision, int log2n) {
       },
       {
           {},
-          {tile_variant<double, 2, 4, 4>(), tile_variant<double, 2, 2, 8>()},
-          {tile_variant<double, 4, 2, 4>(), tile_variant<double, 4, 1, 8>()},
-          {tile_variant<double, 8, 1, 4>(), tile_variant<double, 8, 2, 4>()},
-          {tile_variant<double, 16, 1, 4>(), stockham_variant<double, 16, 8, 64, 2>()},
+          {tile_variant<double, 2, 4, 4, true>(), tile_variant<double, 2, 2, 8>()},
+          {tile_variant<double, 4, 2, 4, true>(), tile_variant<double, 4, 1, 8>()},
+          {tile_variant<double, 8, 1, 4, true>(), tile_variant<double, 8, 2, 4>()},
+          {tile_variant<double, 16, 1, 4, true>(), stockham_variant<double, 16, 8, 64, 2>()},
           {stockham_variant<double, 32, 8, 32, 1, 0, 0, true>(), stockham_variant<double, 32, 8, 32, 2>()},
           {stockham_variant<double, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<double, 64, 8, 16, 2>()},
           {stockham_variant<double, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<double, 128, 8, 8, 1>()},
@@ -583,8 +590,10 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
     }
   }
   e = p->v->prepare[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
-  if (e == cudaSuccess && p->v->prepare_real[direction])  // LDG loader: the LDG carveout rule
-    e = p->v->prepare_real[direction](carveout_override() >= -1 ? carveout_override() : 50);
+  if (e == cudaSuccess && p->v->prepare_real[direction])  // stockham: LDG loader -> LDG carveout rule
+    e = p->v->prepare_real[direction](carveout_override() >= -1                   ? carveout_override()
+                                      : p->v->kernel == SFFT_KERNEL_STOCKHAM ? 50
+                                                                             : -1);
   if (e != cudaSuccess) {
     cudaFree(p->d_tw);
     delete p;

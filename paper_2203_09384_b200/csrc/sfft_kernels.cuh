@@ -529,17 +529,49 @@ __device__ __forceinline__ void seq_dft(cx_t<T> (&x)[N], uint32_t& bad, bool che
   }
 }
 
-template <typename T, int N, int SPT, int WARPS, bool INV>
+// 16-byte chunk of real input -> complex elements with zero imaginary parts
+template <typename C>
+__device__ __forceinline__ void chunk_to_reals(float4 f, C* dst);
+template <>
+__device__ __forceinline__ void chunk_to_reals<float2>(float4 f, float2* dst) {
+  dst[0] = make_float2(f.x, 0.f);
+  dst[1] = make_float2(f.y, 0.f);
+  dst[2] = make_float2(f.z, 0.f);
+  dst[3] = make_float2(f.w, 0.f);
+}
+template <>
+__device__ __forceinline__ void chunk_to_reals<double2>(float4 f, double2* dst) {
+  const double2 d = *reinterpret_cast<const double2*>(&f);
+  dst[0] = make_double2(d.x, 0.0);
+  dst[1] = make_double2(d.y, 0.0);
+}
+
+// Shared memory per warp tile, in 16-byte chunks: the complex tile (staged
+// input and output in place), plus a separate input tile for real input.
+template <typename T, int N, int SPT, bool RIN>
+__host__ __device__ constexpr int tile_chunks() {
+  constexpr int K = N * int(sizeof(cx_t<T>)) / 16;
+  constexpr int KI = RIN ? N * int(sizeof(T)) / 16 : 0;
+  return K == 1 ? 0 : 32 * SPT * (K + KI);
+}
+
+// RIN: real input rows (see stockham_kernel); fp32 N = 2 reads one 8-byte
+// pair per sequence directly, the other sizes stage the real tile in its
+// own shared region and write the complex results to the output region.
+template <typename T, int N, int SPT, int WARPS, bool INV, bool RIN = false>
 __global__ void __launch_bounds__(32 * WARPS)
-tile_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out, long long batch,
+tile_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out, long long batch,
             int* __restrict__ nonfinite) {
   using C = cx_t<T>;
   constexpr int E = sizeof(C);
   constexpr int EPC = 16 / E;         // elements per 16-byte chunk
-  constexpr int K = N / EPC;          // chunks per sequence
+  constexpr int K = N / EPC;          // output (complex) chunks per sequence
   static_assert(K >= 1 && N % EPC == 0, "tile geometry");
-  constexpr int TILE_CH = 32 * SPT * K;  // chunks per warp tile
-  constexpr int CPL = SPT * K;           // chunks per lane
+  constexpr int RPC = 16 / int(sizeof(T));   // reals per chunk
+  constexpr int KI = RIN ? N / RPC : K;      // input chunks per sequence (0: fp32 N=2 real)
+  constexpr int TILE_CH = 32 * SPT * K;      // output chunks per warp tile
+  constexpr int TILE_IN = 32 * SPT * KI;     // input chunks per warp tile
+  constexpr int CPL = SPT * K;               // output chunks per lane
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -558,7 +590,12 @@ tile_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out, long long
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
       const long long c = ch0 + lane + 32 * i;
-      f[i] = c < total_ch ? ld_stream(gin + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (RIN) {  // fp32 N = 2: one float2 of reals per sequence
+        const float2 r = c < total_ch ? ld_stream(reinterpret_cast<const float2*>(in) + c) : make_float2(0.f, 0.f);
+        f[i] = make_float4(r.x, 0.f, r.y, 0.f);
+      } else {
+        f[i] = c < total_ch ? ld_stream(gin + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
@@ -574,15 +611,18 @@ tile_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out, long long
     }
   } else {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4* ws = reinterpret_cast<float4*>(smem_raw) + warp * TILE_CH;
+    float4* ws = reinterpret_cast<float4*>(smem_raw) + warp * tile_chunks<T, N, SPT, RIN>();
+    float4* wi = RIN ? ws + TILE_CH : ws;  // staged input
+    const long long total_in = batch * KI;
+    const long long ci0 = tile * TILE_IN;
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) {
+    for (int i = 0; i < SPT * KI; ++i) {
       const int c = lane + 32 * i;
-      const long long gc = ch0 + c;
-      if (gc < total_ch) {
-        cp_async16(ws + swz_chunk(c), gin + gc);
+      const long long gc = ci0 + c;
+      if (gc < total_in) {
+        cp_async16(wi + swz_chunk(c), gin + gc);
       } else {
-        ws[swz_chunk(c)] = make_float4(0.f, 0.f, 0.f, 0.f);
+        wi[swz_chunk(c)] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     cp_async_wait_all();
@@ -591,8 +631,13 @@ tile_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out, long long
     for (int u = 0; u < SPT; ++u) {
       const int q = u * 32 + lane;  // sequence within the tile
       C x[N];
+      if constexpr (RIN) {
 #pragma unroll
-      for (int c = 0; c < K; ++c) chunk_to_cx<C>(ws[swz_chunk(q * K + c)], x + c * EPC);
+        for (int c = 0; c < KI; ++c) chunk_to_reals<C>(wi[swz_chunk(q * KI + c)], x + c * RPC);
+      } else {
+#pragma unroll
+        for (int c = 0; c < K; ++c) chunk_to_cx<C>(ws[swz_chunk(q * K + c)], x + c * EPC);
+      }
       seq_dft<T, N, INV>(x, bad, check);
 #pragma unroll
       for (int c = 0; c < K; ++c) ws[swz_chunk(q * K + c)] = cx_to_chunk<C>(x + c * EPC);

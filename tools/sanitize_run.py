@@ -37,4 +37,8 @@ for prec in ("single", "double"):
                 torch.cuda.synchronize()
                 assert torch.equal(buf, y)
                 count += 1
+                if plan.supports_real_input(0):  # real-input loader of the default kernels
+                    xr = x.real.contiguous()
+                    assert torch.equal(sf.execute(plan, xr), sf.execute(plan, xr.to(x.dtype)))
+                    count += 1
 print(f"sanitize_run: {count} launches OK")
