@@ -61,7 +61,7 @@ struct Variant {
   LaunchFn launch[2];    // [direction]
   PrepareFn prepare[2];  // [direction]
   // real-valued input rows (imaginary parts zero), default variants only;
-  // always the per-thread (LDG) loader with the LDG carveout
+  // same loader and carveout as the complex kernel
   LaunchFn launch_real[2];
   PrepareFn prepare_real[2];
 };
@@ -219,10 +219,10 @@ Variant stockham_variant() {
   v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   if constexpr (REAL) {
-    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, 0, true>;
-    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, 0, true>;
-    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, 0, true>;
-    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, 0, true>;
+    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
+    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
+    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
+    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
   }
   return v;
 }
@@ -590,10 +590,8 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
     }
   }
   e = p->v->prepare[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
-  if (e == cudaSuccess && p->v->prepare_real[direction])  // stockham: LDG loader -> LDG carveout rule
-    e = p->v->prepare_real[direction](carveout_override() >= -1                   ? carveout_override()
-                                      : p->v->kernel == SFFT_KERNEL_STOCKHAM ? 50
-                                                                             : -1);
+  if (e == cudaSuccess && p->v->prepare_real[direction])  // same loader, same carveout rule
+    e = p->v->prepare_real[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
   if (e != cudaSuccess) {
     cudaFree(p->d_tw);
     delete p;

@@ -332,12 +332,11 @@ __device__ __forceinline__ void pdl_enter() {
 //           shared memory -- no per-thread global loads at all.
 // RIN: the input rows are real (N values of T each, imaginary parts zero) --
 //      the C2C transform of a real signal reads 4 (8) bytes per element
-//      instead of 8 (16) and needs no separate widening pass (LOADER 0 only).
+//      instead of 8 (16) and needs no separate widening pass.
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0, bool RIN = false>
 __global__ void __launch_bounds__((N / R) * SEQ)
 stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
                 const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
-  static_assert(!RIN || LOADER == 0, "real input uses the per-thread loader");
   using C = cx_t<T>;
   using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
@@ -362,7 +361,7 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
     const long long nseq = batch - seq0 < SEQ ? batch - seq0 : SEQ;
     if (tid == 0) {
       mbar_init(&bar, 1);
-      const uint32_t bytes = uint32_t(nseq * N * int(sizeof(C)));
+      const uint32_t bytes = uint32_t(nseq * N * int(sizeof(*in)));
       mbar_expect_tx(&bar, bytes);
       bulk_g2s(sm, in + seq0 * N, bytes, &bar);
     }
@@ -370,8 +369,14 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
     mbar_wait(&bar, 0);
     // rows past the batch read stale staging; they are never stored and are
     // excluded from the non-finite check below
+    if constexpr (RIN) {
+      const T* smr = reinterpret_cast<const T*>(smem_raw);
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = sm[s * N + j + m * G];  // linear staging, conflict-free
+      for (int m = 0; m < R; ++m) v[m] = C{smr[s * N + j + m * G], T(0)};
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = sm[s * N + j + m * G];  // linear staging, conflict-free
+    }
     __syncthreads();  // staging fully read before the exchange layout reuses it
   } else {
     // rows past the batch (last CTA only) re-read the last row instead of
