@@ -3,6 +3,7 @@
 // reference interfaces each entry point replaces.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -132,16 +133,16 @@ constexpr int pipe_smem() {
 // persistent grid.  Cached per kernel instantiation and device.
 template <typename K>
 int persistent_grid(K kernel, int threads, int smem) {
-  static int cached[16] = {};
+  static std::atomic<int> cached[16] = {};  // racing writers store the same value
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return 0;
-  if (cached[dev] > 0) return cached[dev];
+  if (const int c = cached[dev].load(std::memory_order_relaxed); c > 0) return c;
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) return 0;
   if (per_sm < 1) per_sm = 1;
-  cached[dev] = sms * per_sm;
-  return cached[dev];
+  cached[dev].store(sms * per_sm, std::memory_order_relaxed);
+  return sms * per_sm;
 }
 
 template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
@@ -896,6 +897,12 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
       p->h_chunk_bytes = stage_bytes;
     }
     auto& pool = sfft_host::CopyPool::instance();
+    // a failure mid-pipeline drains the streams before returning, so the next
+    // call never races leftover copies on the slot buffers
+    auto fail_sync = [&](cudaError_t err, const char* what) {
+      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
+      return cuda_fail(err, what);
+    };
     // staged (pageable) path: which rows each slot's host staging holds
     int64_t slot_row[kMaxHostStreams] = {}, slot_rows[kMaxHostStreams] = {};
     auto drain_slot = [&](int s) -> cudaError_t {
@@ -919,7 +926,7 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
         // the slot's previous chunk must have left the host staging (its D2H
         // done implies its H2D done)
         e = drain_slot(s);
-        if (e != cudaSuccess) return cuda_fail(e, "staging drain");
+        if (e != cudaSuccess) return fail_sync(e, "staging drain");
         pool.memcpy(p->h_chunk_in[s], src + row * in_row_bytes, in_bytes);
         h2d_src = p->h_chunk_in[s];
         d2h_dst = p->h_chunk_out[s];
@@ -927,17 +934,17 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
       if (reuse) e = cudaStreamWaitEvent(p->st_h2d, p->ev_k[s], 0);
       if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_in[s], h2d_src, in_bytes, cudaMemcpyHostToDevice, p->st_h2d);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_h2d[s], p->st_h2d);
-      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+      if (e != cudaSuccess) return fail_sync(e, "H2D copy");
       e = cudaStreamWaitEvent(p->st_kernel, p->ev_h2d[s], 0);
       if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(p->st_kernel, p->ev_d2h[s], 0);
       if (e == cudaSuccess)
         e = launch(p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel, false);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[s], p->st_kernel);
-      if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+      if (e != cudaSuccess) return fail_sync(e, "kernel launch");
       e = cudaStreamWaitEvent(p->st_d2h, p->ev_k[s], 0);
       if (e == cudaSuccess) e = cudaMemcpyAsync(d2h_dst, p->d_out[s], bytes, cudaMemcpyDeviceToHost, p->st_d2h);
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_d2h[s], p->st_d2h);
-      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+      if (e != cudaSuccess) return fail_sync(e, "D2H copy");
       if (!pinned) {
         slot_row[s] = row;
         slot_rows[s] = rows;
@@ -947,7 +954,7 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
       // drain in chunk order (oldest first)
       for (int k = 0; k < S; ++k) {
         e = drain_slot((chunk + k) % S);
-        if (e != cudaSuccess) return cuda_fail(e, "staging drain");
+        if (e != cudaSuccess) return fail_sync(e, "staging drain");
       }
     }
     for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) {
