@@ -170,9 +170,13 @@ def _prepare_device(plan: FftPlan, x):
 def launch(plan: FftPlan, x_in, x_out, rows: int, *, stream=None, flag=None) -> None:
     """Asynchronous launch on device tensors (no validation, no sync).
 
-    ``x_in``/``x_out`` are contiguous CUDA tensors of the plan dtype holding
-    ``rows`` sequences; ``flag`` an int32 CUDA tensor the kernel ORs 1 into on
-    NaN/Inf input.  This is the call ``bench.py`` times.
+    ``x_in``/``x_out`` are contiguous CUDA tensors holding ``rows``
+    sequences: ``x_out`` of the plan dtype, ``x_in`` of the plan dtype or of
+    its real type (float32 / float64 rows, read by the real-input loader);
+    ``flag`` an int32 CUDA tensor the kernel ORs 1 into on NaN/Inf input.
+    Kernels are launched with programmatic dependent launch, so back-to-back
+    calls overlap one launch's ramp with the previous one's drain while
+    staying ordered.  This is the call ``bench.py`` times.
     """
     dev = x_in.get_device()
     raw = _raw_stream(dev) if stream is None else stream.cuda_stream
