@@ -281,9 +281,11 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<float, 8, 4, 4, true>(), tile_variant<float, 8, 2, 4>()},
           {tile_variant<float, 16, 2, 4, true>(), tile_variant<float, 16, 1, 8>()},
           {tile_variant<float, 32, 1, 4, true>(), stockham_variant<float, 32, 8, 32, 1>()},
-          {stockham_variant<float, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<float, 64, 16, 32, 1>()},
-          {stockham_variant<float, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<float, 128, 16, 16, 1>(),
-           stockham_variant<float, 128, 8, 8, 1>()},
+          {stockham_variant<float, 64, 8, 16, 1, 1, 0, true>(), stockham_variant<float, 64, 16, 32, 1>(),
+           stockham_variant<float, 64, 8, 16, 1>()},
+          {stockham_variant<float, 128, 16, 16, 1, 1, 0, true>(), stockham_variant<float, 128, 16, 16, 1>(),
+           stockham_variant<float, 128, 8, 8, 1>(), stockham_variant<float, 128, 16, 16, 2, 1>(),
+           stockham_variant<float, 128, 16, 16, 2>()},
           {stockham_variant<float, 256, 16, 8, 1, 0, 0, true>(), stockham_variant<float, 256, 16, 8, 2>(),
            stockham_variant<float, 256, 16, 8, 1, 1>(), stockham_variant<float, 256, 16, 8, 1, 0, 1>()},
           {stockham_variant<float, 512, 16, 4, 1, 1, 0, true>(), stockham_variant<float, 512, 16, 2, 1>(),
@@ -304,9 +306,12 @@ const std::vector<Variant>& variants(int precision, int log2n) {
           {tile_variant<double, 4, 2, 4, true>(), tile_variant<double, 4, 1, 8>()},
           {tile_variant<double, 8, 1, 4, true>(), tile_variant<double, 8, 2, 4>()},
           {tile_variant<double, 16, 1, 4, true>(), stockham_variant<double, 16, 8, 64, 2>()},
-          {stockham_variant<double, 32, 8, 32, 1, 0, 0, true>(), stockham_variant<double, 32, 8, 32, 2>()},
-          {stockham_variant<double, 64, 8, 16, 1, 0, 0, true>(), stockham_variant<double, 64, 8, 16, 2>()},
-          {stockham_variant<double, 128, 16, 16, 2, 0, 0, true>(), stockham_variant<double, 128, 8, 8, 1>()},
+          {stockham_variant<double, 32, 8, 32, 1, 1, 0, true>(), stockham_variant<double, 32, 8, 32, 2>(),
+           stockham_variant<double, 32, 8, 32, 1>()},
+          {stockham_variant<double, 64, 8, 16, 1, 1, 0, true>(), stockham_variant<double, 64, 8, 16, 2>(),
+           stockham_variant<double, 64, 8, 16, 1>()},
+          {stockham_variant<double, 128, 16, 16, 2, 1, 0, true>(), stockham_variant<double, 128, 8, 8, 1>(),
+           stockham_variant<double, 128, 16, 16, 2>()},
           {stockham_variant<double, 256, 16, 8, 2, 1, 0, true>(), stockham_variant<double, 256, 8, 4, 1>(),
            stockham_variant<double, 256, 16, 8, 2>()},
           {stockham_variant<double, 512, 16, 4, 2, 1, 0, true>(), stockham_variant<double, 512, 16, 2, 2>(),
