@@ -288,8 +288,9 @@ const std::vector<Variant>& variants(int precision, int log2n) {
            stockham_variant<float, 128, 16, 16, 2>()},
           {stockham_variant<float, 256, 16, 8, 1, 0, 0, true>(), stockham_variant<float, 256, 16, 8, 2>(),
            stockham_variant<float, 256, 16, 8, 1, 1>(), stockham_variant<float, 256, 16, 8, 1, 0, 1>()},
-          {stockham_variant<float, 512, 16, 4, 1, 1, 0, true>(), stockham_variant<float, 512, 16, 2, 1>(),
-           stockham_variant<float, 512, 16, 4, 1>()},
+          {stockham_variant<float, 512, 32, 4, 1, 1, 0, true>(), stockham_variant<float, 512, 16, 2, 1>(),
+           stockham_variant<float, 512, 16, 4, 1>(), stockham_variant<float, 512, 16, 4, 1, 1>(),
+           stockham_variant<float, 512, 32, 8, 1, 1>()},
           {stockham_variant<float, 1024, 32, 2, 1, 1, 0, true>(), stockham_variant<float, 1024, 16, 1, 1, 1, 1>(),
            stockham_variant<float, 1024, 16, 1, 1, 1>(), stockham_variant<float, 1024, 16, 1, 1>(),
            stockham_variant<float, 1024, 32, 4, 1>(), stockham_variant<float, 1024, 16, 2, 1>(),
