@@ -25,7 +25,7 @@ def timed(fn, iters=10, rounds=5):
 for prec in ("single", "double"):
     rdt, cdt = (torch.float32, torch.complex64) if prec == "single" else (torch.float64, torch.complex128)
     resz = 4 if prec == "single" else 8
-    for n in (2, 8, 32, 64, 256, 1024, 2048):
+    for n in [int(a) for a in os.environ.get("NS", "2,8,32,64,256,1024,2048").split(",")]:
         rows = (1 << 30) // (n * 2 * resz)
         xr = torch.rand((rows, n), dtype=rdt, device="cuda")
         y = torch.empty((rows, n), dtype=cdt, device="cuda")
