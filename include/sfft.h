@@ -134,7 +134,8 @@ int sfft_execute_sync(sfft_plan_t plan, const void* d_in, void* d_out, int64_t b
 
 /* Input kinds of the _ex entry points.  SFFT_INPUT_REAL: `d_in` holds
  * `batch` rows of n REAL values (float for SFFT_SINGLE, double for
- * SFFT_DOUBLE; element-aligned) -- the C2C transform of a real signal, as
+ * SFFT_DOUBLE; 16-byte aligned like complex input -- the real loaders read
+ * 16-byte chunks of reals) -- the C2C transform of a real signal, as
  * the reference computes for real input (executor.py:74 casts it to
  * complex; tests/test_executor.py:89-92).  The kernel reads the reals and
  * zero imaginary parts in registers: half the input traffic, no widening

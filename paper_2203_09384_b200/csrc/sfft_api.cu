@@ -711,11 +711,13 @@ LaunchFn pick_launch(sfft_plan_t p, int32_t input_kind, const void* d_in, const 
     *rc = fail(SFFT_ERR_ARGUMENT, "input_kind must be SFFT_INPUT_COMPLEX or SFFT_INPUT_REAL");
     return nullptr;
   }
-  const uintptr_t in_align = input_kind == SFFT_INPUT_REAL ? (p->precision == SFFT_SINGLE ? 4u : 8u) : 16u;
-  if ((reinterpret_cast<uintptr_t>(d_in) % in_align) | (reinterpret_cast<uintptr_t>(d_out) & 15u)) {
-    *rc = fail(SFFT_ERR_ARGUMENT, input_kind == SFFT_INPUT_REAL
-                                      ? "real input must be element-aligned and output 16-byte aligned"
-                                      : "data pointers must be 16-byte aligned");
+  // Both input kinds need 16-byte alignment: the complex loaders move 8- or
+  // 16-byte elements, and the real loaders read 16-byte chunks of reals
+  // (tile kernels: cp.async 16; fp32 N = 2: 8-byte pairs; bulk TMA: 16-byte
+  // source alignment).  A real row view at a 4- or 8-byte offset is refused
+  // here instead of faulting in the kernel (the Python layer re-copies it).
+  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u) {
+    *rc = fail(SFFT_ERR_ARGUMENT, "data pointers must be 16-byte aligned (input and output)");
     return nullptr;
   }
   if (input_kind == SFFT_INPUT_COMPLEX) return p->v->launch[p->direction];

@@ -160,6 +160,8 @@ def _prepare_device(plan: FftPlan, x):
     single = plan.dtype == np.complex64
     if not x.is_complex() and plan.supports_real_input(x.get_device()):
         xr = x.to(torch.float32 if single else torch.float64).contiguous()
+        if xr.data_ptr() % 16:  # the real loaders read 16-byte chunks (sfft.h)
+            xr = xr.clone()
         return xr, rows, _native.SFFT_INPUT_REAL
     xc = x.to(torch.complex64 if single else torch.complex128).contiguous()
     if xc.data_ptr() % 16:

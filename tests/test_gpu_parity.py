@@ -227,6 +227,41 @@ def test_misaligned_view(cuda):
     assert np.array_equal(got, sf.execute(plan, view.cpu().numpy()))
 
 
+@pytest.mark.parametrize(
+    "n,prec,offset",
+    [(2, "single", 1), (8, "single", 1), (8, "single", 3), (32, "single", 2), (2048, "single", 1),
+     (8, "double", 1), (1024, "double", 1), (2048, "double", 1)],
+)
+def test_misaligned_real_view(cuda, n, prec, offset):
+    """Real rows at a 4-byte (fp32) or 8-byte (fp64) offset: the tile, bulk-TMA
+    and vectorised real loaders read 16-byte chunks.  execute() re-copies the
+    view (bit-identical to an aligned copy); the raw entry points refuse it
+    with SFFT_ERR_ARGUMENT instead of faulting -- and the context stays usable."""
+    rdt = torch.float32 if prec == "single" else torch.float64
+    rows = 37
+    flat = torch.from_numpy(sf.generate_batch(1, offset + rows * n, seed=5, precision=prec).real.copy())
+    flat = flat.to(rdt).to(cuda).reshape(-1)
+    view = flat[offset:].reshape(rows, n)
+    assert view.data_ptr() % 16 != 0
+    plan = sf.make_plan(n, precision=prec)
+    got = sf.execute(plan, view)
+    aligned = view.clone()
+    assert aligned.data_ptr() % 16 == 0
+    want = sf.execute(plan, aligned)
+    assert torch.equal(got, want)
+    # widening to complex first gives the same bits (real loader == widening)
+    assert torch.equal(got, sf.execute(plan, aligned.to(got.dtype)))
+    out = torch.empty_like(want)
+    with pytest.raises(sf.FftError, match="16-byte aligned"):
+        sf.launch(plan, view, out, rows)
+    lib = sf._native.lib()
+    rc = lib.sfft_execute_ex(plan.native_handle(cuda.index or 0), view.data_ptr(), out.data_ptr(), rows,
+                             None, None, sf._native.SFFT_INPUT_REAL)
+    assert rc == 7  # SFFT_ERR_ARGUMENT
+    torch.cuda.synchronize()
+    assert torch.equal(sf.execute(plan, view), want)  # no sticky fault
+
+
 def test_shared_plan_across_threads(cuda):
     from concurrent.futures import ThreadPoolExecutor
 
