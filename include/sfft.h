@@ -167,7 +167,8 @@ int sfft_execute_host_ex(sfft_plan_t plan, const void* h_in, void* h_out, int64_
  * but the reference's building blocks for custom stage lists.
  *
  * sfft_permute: out[r, p] = in[r, perm[p]] for `batch` rows of n elements
- *   (the digit-reversal load of executor.py:77); perm is int64 on device.
+ *   (the digit-reversal load of executor.py:77); perm is int64 on device;
+ *   an entry outside [0, n) reads nothing and yields NaN in that slot.
  * sfft_stage: one out-of-place radix-2/4/8 decimation-in-time stage over
  *   sub-spectra of length `stride`; operand (q, j) of each group is scaled
  *   by table[(n/(radix*stride))*q*j mod n] (conjugated for SFFT_INVERSE);

@@ -21,7 +21,15 @@ from .errors import (
     UnsupportedLengthError,
 )
 from .executor import TimedExecution, execute, execute_timed, launch
-from .kernels import count_butterflies, split_radix_transform
+from .kernels import (
+    StageBuffer,
+    count_butterflies,
+    digit_reverse,
+    radix2_stage,
+    radix4_stage,
+    radix8_stage,
+    split_radix_transform,
+)
 from .numerics import TABLE_MAX_LENGTH, TwiddleTable, build_twiddle_table, is_power_of_two, twiddle
 from .planner import (
     ENGINE_MAX_LENGTH,
@@ -37,7 +45,7 @@ from .planner import (
     make_plan,
 )
 from . import sharding
-from .protocol import (
+from .bench import (
     BenchmarkRecord,
     BenchmarkResult,
     BenchmarkSummary,
@@ -50,21 +58,21 @@ from .protocol import (
 )
 from .sharding import execute_sharded, max_over_ranks, shard_bounds
 from .sigio import read_signal, write_signal
-from .verify import (
+from .oracle import dft_matrix, naive_dft, naive_dft_batch
+from .stats import (
+    BatchReport,
     ChiSquareReport,
     Histogram,
     build_histograms,
     chi2_p_value,
     chi2_reduced,
     compare_spectra,
-    dft_matrix,
     lower_regularized_gamma,
-    naive_dft,
     relative_difference,
     upper_regularized_gamma,
     verify_batch,
 )
-from .stages import StageBuffer, digit_reverse, radix2_stage, radix4_stage, radix8_stage
+from .validation import COMPLEX_DTYPE, as_signal, check_same_length, check_signal_matrix
 from .signalgen import KINDS, generate, generate_batch
 
 try:
@@ -77,10 +85,12 @@ __version__ = "0.1.0"
 __all__ = [
     "Algorithm",
     "ArgumentError",
+    "BatchReport",
     "BenchmarkRecord",
     "BenchmarkResult",
     "BenchmarkSummary",
     "ChiSquareReport",
+    "COMPLEX_DTYPE",
     "CudaError",
     "Direction",
     "DomainError",
@@ -103,10 +113,13 @@ __all__ = [
     "TimedExecution",
     "TwiddleTable",
     "UnsupportedLengthError",
+    "as_signal",
     "build_histograms",
     "build_twiddle_table",
     "chi2_p_value",
     "chi2_reduced",
+    "check_same_length",
+    "check_signal_matrix",
     "compare_spectra",
     "count_butterflies",
     "dft_matrix",
@@ -128,6 +141,7 @@ __all__ = [
     "make_plan",
     "max_over_ranks",
     "naive_dft",
+    "naive_dft_batch",
     "radix2_stage",
     "radix4_stage",
     "radix8_stage",

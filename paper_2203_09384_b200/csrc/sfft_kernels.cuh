@@ -174,11 +174,32 @@ __host__ __device__ constexpr int high_pow2(int q) {
 // TWP 0: every w^q is its own table entry (r-1 loads, exact table values).
 // TWP 1: only w^(2^i) are loaded; w^q = w^hi * w^(q-hi) (<= 3 products deep,
 //        error <= ~3 ulp) -- trades L1 wavefronts for FMA-pipe work.
+// TWP 2: two-level, w^q = w^(q - q mod S) * w^(q mod S) with both factors
+//        loaded (S = 4, or 8 for r = 32): one product deep (~1 ulp, against
+//        ~3 for TWP 1), fewer products than TWP 1, a few more loads.  At
+//        r = 16: 6 loads + 9 products (TWP 1: 4 + 11; TWP 0: 15 + 0).
+template <int r>
+__host__ __device__ constexpr int twiddle_split() {
+  return r >= 32 ? 8 : 4;
+}
 template <int TWP, int r, int L, int NB, typename C, int R>
 __device__ __forceinline__ void apply_pass_twiddles(C (&v)[R], const C* __restrict__ tp, int t) {
   if constexpr (TWP == 0) {
 #pragma unroll
     for (int q = 1; q < r; ++q) v[t + q * NB] = cmul(v[t + q * NB], __ldg(tp + (q - 1) * L));
+  } else if constexpr (TWP == 2) {
+    constexpr int S = twiddle_split<r>();
+    C w[r];
+    static_for<1, r>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int lo = q % S;
+      if constexpr (lo == 0 || q < S) {
+        w[q] = __ldg(tp + (q - 1) * L);
+      } else {
+        w[q] = cmul(w[q - lo], w[lo]);
+      }
+      v[t + q * NB] = cmul(v[t + q * NB], w[q]);
+    });
   } else {
     C w[r];
     static_for<1, r>([&](auto Q) {

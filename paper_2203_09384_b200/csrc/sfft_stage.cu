@@ -97,7 +97,11 @@ __global__ void gather_kernel(const sfft::cx_t<T>* __restrict__ in, sfft::cx_t<T
   if (tid >= total) return;
   const long long row = tid / n;
   const int p = int(tid - row * n);
-  out[tid] = in[row * n + perm[p]];
+  const long long q = perm[p];
+  // an out-of-range entry never reads outside its row: it yields NaN (sfft.h)
+  out[tid] = (unsigned long long)q < (unsigned long long)n
+                 ? in[row * n + q]
+                 : sfft::cx_t<T>{T(__int_as_float(0x7fc00000)), T(__int_as_float(0x7fc00000))};
 }
 
 template <typename T>

@@ -1,0 +1,261 @@
+// Kernel variants: the launch/prepare entry points of every compiled
+// instantiation and the Variant records the planner picks from.  Included by
+// sfft_api.cu and by the per-(precision, N) table translation units
+// (sfft_table_*.cu), which instantiate the kernels in parallel builds.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/sfft.h"
+#include "sfft_kernels.cuh"
+
+namespace sfft_impl {
+
+// pdl: launch with programmatic stream serialization (see launch_pdl)
+using LaunchFn = cudaError_t (*)(const void* in, void* out, const void* tw, long long batch,
+                                 int* flag, cudaStream_t st, bool pdl);
+using PrepareFn = cudaError_t (*)(int carveout);
+
+struct Variant {
+  int kernel;      // SFFT_KERNEL_*
+  int r;           // elements per thread (stockham R; tile: n)
+  int seq;         // sequences per CTA
+  int layout;      // smem layout (stockham): 0 xor swizzle, 1 padded
+  int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products
+  int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA,
+                   // 2 persistent CTAs with a `stages`-deep bulk TMA pipeline
+  int stages;      // loader 2: shared-memory stage buffers per CTA
+  int carveout;    // preferred shared-memory carveout, % of max (-1: driver default)
+  int threads;     // threads per CTA
+  int smem;        // dynamic smem bytes
+  int passes;
+  int radices[8];
+  int tw_len;      // per-pass twiddle elements
+  LaunchFn launch[2];    // [direction]
+  PrepareFn prepare[2];  // [direction]
+  // real-valued input rows (imaginary parts zero), default variants only;
+  // same loader and carveout as the complex kernel
+  LaunchFn launch_real[2];
+  PrepareFn prepare_real[2];
+};
+
+// ---------------------------------------------------------------- launchers
+template <typename T, int N, int R, int SEQ, int LAYOUT>
+constexpr int stockham_smem() {
+  return SEQ * sfft::Smem<T, LAYOUT, R>::size(N) * int(sizeof(sfft::cx_t<T>));
+}
+
+// SFFT_PDL=0 disables programmatic dependent launch (A/B and debugging).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SFFT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+// (the kernels call griddepcontrol.wait before any global access).
+// Used for launches on the caller's stream; the host pipeline, whose kernels
+// follow cross-stream event waits, launches with pdl = false.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), long long grid, int threads, int smem, cudaStream_t st,
+                       Args... args) {
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
+cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
+                            cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
+  constexpr int threads = (N / R) * SEQ;
+  constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
+  const long long grid = (batch + SEQ - 1) / SEQ;
+  return launch_pdl(pdl, sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>, grid, threads, smem,
+                    st, static_cast<const In*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
+}
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
+cudaError_t prepare_stockham(int carveout) {
+  const auto k = sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       stockham_smem<T, N, R, SEQ, LAYOUT>());
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+
+// ------------------------------------------------- persistent pipeline
+template <typename T, int N, int R, int SEQ, int LAYOUT, int STAGES>
+constexpr int pipe_smem() {
+  return STAGES * stockham_smem<T, N, R, SEQ, LAYOUT>();
+}
+
+// Resident CTAs of `kernel` on the current device, times its SM count: the
+// persistent grid.  `cache` belongs to one kernel instantiation (a static of
+// the launcher template below), so two pipelined kernels of the same
+// signature never share a grid size.
+template <typename K>
+int persistent_grid(K kernel, int threads, int smem, std::atomic<int> (&cache)[16]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return 0;
+  if (const int c = cache[dev].load(std::memory_order_relaxed); c > 0) return c;
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) return 0;
+  if (per_sm < 1) per_sm = 1;
+  cache[dev].store(sms * per_sm, std::memory_order_relaxed);  // racing writers store the same value
+  return sms * per_sm;
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
+cudaError_t launch_stockham_pipe(const void* in, void* out, const void* tw, long long batch, int* flag,
+                                 cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  constexpr int threads = (N / R) * SEQ;
+  constexpr int smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
+  const auto k = sfft::stockham_pipe_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, STAGES>;
+  const long long tiles = (batch + SEQ - 1) / SEQ;
+  static std::atomic<int> grid_cache[16] = {};  // per instantiation
+  const int full = persistent_grid(k, threads, smem, grid_cache);
+  if (full <= 0) return cudaErrorInvalidConfiguration;
+  const long long grid = tiles < full ? tiles : full;
+  return launch_pdl(pdl, k, grid, threads, smem, st, static_cast<const C*>(in), static_cast<C*>(out),
+                    static_cast<const C*>(tw), batch, flag);
+}
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int STAGES>
+cudaError_t prepare_stockham_pipe(int carveout) {
+  const auto k = sfft::stockham_pipe_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>());
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+
+template <typename T, int N, int SPT, int W, bool RIN = false>
+constexpr int tile_smem() {
+  return W * sfft::tile_chunks<T, N, SPT, RIN>() * 16;
+}
+
+template <typename T, int N, int SPT, int W, bool INV, bool RIN = false>
+cudaError_t launch_tile(const void* in, void* out, const void*, long long batch, int* flag,
+                        cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
+  constexpr int smem = tile_smem<T, N, SPT, W, RIN>();
+  constexpr long long per_cta = 32LL * SPT * W;
+  const long long grid = (batch + per_cta - 1) / per_cta;
+  return launch_pdl(pdl, sfft::tile_kernel<T, N, SPT, W, INV, RIN>, grid, 32 * W, smem, st,
+                    static_cast<const In*>(in), static_cast<C*>(out), batch, flag);
+}
+template <typename T, int N, int SPT, int W, bool INV, bool RIN = false>
+cudaError_t prepare_tile(int carveout) {
+  constexpr int smem = tile_smem<T, N, SPT, W, RIN>();
+  const auto k = sfft::tile_kernel<T, N, SPT, W, INV, RIN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+
+template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0, bool REAL = false>
+Variant stockham_variant() {
+  Variant v{};
+  v.kernel = SFFT_KERNEL_STOCKHAM;
+  v.r = R;
+  v.seq = SEQ;
+  v.layout = LAYOUT;
+  v.threads = (N / R) * SEQ;
+  v.smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
+  v.passes = sfft::num_passes(N, R);
+  for (int p = 0; p < v.passes && p < 8; ++p) v.radices[p] = sfft::pass_radix(N, R, p);
+  v.tw_len = sfft::twiddle_table_len(N, R);
+  v.twp = TWP;
+  v.loader = LOADER;
+  // Per-thread global loads land in L1 before they reach registers, so every
+  // LDG line in flight holds L1 capacity.  Left to the driver, a variant
+  // whose resident CTAs fill the smem carveout (e.g. 12 x 16.9 KB -> 228 KB,
+  // 28 KB of L1) starves its own loads: 5.6 instead of 6.9-7.0 TB/s
+  // (tools/probe/occ_probe.cu, profiles/r01_occ_probe.txt).  Capping shared
+  // memory at half the unified 256 KB keeps >= 124 KB of L1.  Bulk (TMA)
+  // copies land in shared memory directly and keep the driver default.
+  v.carveout = LOADER == 0 ? 50 : -1;
+  v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
+  v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
+  v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
+  v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
+    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
+    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
+    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
+  }
+  return v;
+}
+
+// persistent pipelined Stockham (loader 2)
+template <typename T, int N, int R, int SEQ, int LAYOUT, int TWP, int STAGES>
+Variant pipe_variant() {
+  Variant v = stockham_variant<T, N, R, SEQ, LAYOUT, TWP, 1>();
+  v.loader = 2;
+  v.stages = STAGES;
+  v.smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
+  v.carveout = -1;  // bulk copies land in shared memory; the driver sizes it
+  v.launch[0] = &launch_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
+  v.launch[1] = &launch_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
+  v.prepare[0] = &prepare_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
+  v.prepare[1] = &prepare_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
+  return v;
+}
+
+template <typename T, int N, int SPT, int W, bool REAL = false>
+Variant tile_variant() {
+  Variant v{};
+  v.kernel = SFFT_KERNEL_TILE;
+  v.r = N;
+  v.seq = 32 * SPT * W;
+  v.threads = 32 * W;
+  v.smem = tile_smem<T, N, SPT, W>();
+  v.passes = 1;
+  v.radices[0] = N;
+  v.tw_len = 0;
+  v.carveout = -1;  // cp.async stages through shared memory, not L1 lines
+  v.launch[0] = &launch_tile<T, N, SPT, W, false>;
+  v.launch[1] = &launch_tile<T, N, SPT, W, true>;
+  v.prepare[0] = &prepare_tile<T, N, SPT, W, false>;
+  v.prepare[1] = &prepare_tile<T, N, SPT, W, true>;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_tile<T, N, SPT, W, false, true>;
+    v.launch_real[1] = &launch_tile<T, N, SPT, W, true, true>;
+    v.prepare_real[0] = &prepare_tile<T, N, SPT, W, false, true>;
+    v.prepare_real[1] = &prepare_tile<T, N, SPT, W, true, true>;
+  }
+  return v;
+}
+
+// Variant tables of one (precision, log2 n) group; entry 0 is the planner's
+// default.  Defined by the sfft_table_*.cu translation units.
+std::vector<Variant> table_f32_small(int log2n);  // N = 2 .. 256
+std::vector<Variant> table_f32_512(int log2n);
+std::vector<Variant> table_f32_1024(int log2n);
+std::vector<Variant> table_f32_2048(int log2n);
+std::vector<Variant> table_f64_small(int log2n);  // N = 2 .. 256
+std::vector<Variant> table_f64_512(int log2n);
+std::vector<Variant> table_f64_1024(int log2n);
+std::vector<Variant> table_f64_2048(int log2n);
+
+}  // namespace sfft_impl

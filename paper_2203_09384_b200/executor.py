@@ -28,8 +28,9 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _native
-from .errors import DomainError, InvalidLengthError, ShapeError
+from .errors import DomainError, ShapeError
 from .planner import FftPlan
+from .validation import check_batch
 
 try:  # torch is the device-memory/stream plumbing; numpy input works without it
     import torch
@@ -65,19 +66,6 @@ def _get_raw_stream_slow(device_index: int) -> int:
 _get_raw_stream = getattr(getattr(torch, "_C", None), "_cuda_getCurrentRawStream", None) or _get_raw_stream_slow
 
 
-def _check_shape(plan: FftPlan, shape) -> int:
-    if len(shape) not in (1, 2):
-        raise ShapeError(f"signal must be (N,) or (batch, N), got shape {tuple(shape)}")
-    if shape[-1] != plan.length:
-        raise ShapeError(f"signal length {shape[-1]} does not match plan length {plan.length}")
-    rows = 1 if len(shape) == 1 else int(shape[0])
-    if rows == 0:
-        raise InvalidLengthError(f"signal batch is empty, shape {tuple(shape)}")
-    if plan.batch is not None and len(shape) == 2 and rows != plan.batch:
-        raise ShapeError(f"signal has {rows} rows; the plan was made for batch={plan.batch}")
-    return rows
-
-
 def _default_device(plan: FftPlan) -> int:
     if plan.device is not None:
         return plan.device
@@ -96,7 +84,7 @@ def _prepare_host(plan: FftPlan, signal, allow_real: bool = False):
     executor.py:74 do (complex128 -> complex64 for a single-precision plan).
     """
     x = np.asarray(signal)
-    rows = _check_shape(plan, x.shape)
+    rows = check_batch(plan.length, x.shape, plan.batch)
     if x.dtype.kind not in "fciu":
         raise DomainError(f"signal has non-numeric dtype {x.dtype}")
     if allow_real and x.dtype.kind != "c" and plan.supports_real_input(_default_device(plan)):
@@ -129,7 +117,11 @@ def _empty_host(shape, dtype) -> np.ndarray:
     return np.frombuffer(m, dtype=dtype).reshape(shape)
 
 
-def _execute_host(plan: FftPlan, signal, out=None):
+def _execute_host(plan: FftPlan, signal, out=None, timed: bool = False):
+    """numpy path; with ``timed``, returns (out, dispatch_us, compute_us) where
+    dispatch covers validation and conversion and compute the native call
+    (H2D copies, kernels and D2H copies of the host pipeline)."""
+    t0 = time.perf_counter_ns()
     x, xc, rows, kind = _prepare_host(plan, signal, allow_real=True)
     if out is None:
         out = _empty_host(xc.shape, plan.dtype)
@@ -142,8 +134,12 @@ def _execute_host(plan: FftPlan, signal, out=None):
     ):
         raise ShapeError("out must be a C-contiguous, 16-byte aligned array of the plan dtype and size")
     handle = plan.native_handle(_default_device(plan))
+    t1 = time.perf_counter_ns()
     _native.check(_native.lib().sfft_execute_host_ex(handle, xc.ctypes.data, out.ctypes.data, rows, kind))
-    return out
+    if not timed:
+        return out
+    t2 = time.perf_counter_ns()
+    return out, (t1 - t0) / 1000.0, (t2 - t1) / 1000.0
 
 
 # ----------------------------------------------------------------- torch path
@@ -154,7 +150,7 @@ def _prepare_device(plan: FftPlan, x):
     goes to the kernel as real rows when its loader supports that: it reads
     half the bytes and zeroes the imaginary parts in registers, instead of a
     widening pass to complex first."""
-    rows = _check_shape(plan, tuple(x.shape))
+    rows = check_batch(plan.length, x.shape, plan.batch)
     if x.dtype == torch.bool:  # numpy kind "b" is rejected too (executor.py:70-71)
         raise DomainError(f"signal has non-numeric dtype {x.dtype}")
     single = plan.dtype == np.complex64
@@ -248,21 +244,16 @@ def execute(plan: FftPlan, signal, *, out=None):
 def execute_timed(plan: FftPlan, signal) -> TimedExecution:
     """execute plus timing (executor.py:55-96).
 
-    ``dispatch_us``: host time from entry to the kernel launch (validation,
-    dtype conversion and, for host input, the H2D copy); ``compute_us``: the
-    kernel's device time from CUDA events recorded around the launch on its
-    stream (sfft_execute_sync).
+    ``dispatch_us``: host time from entry to the native call (validation,
+    dtype conversion, output allocation).  ``compute_us``: for a CUDA tensor,
+    the kernel's device time from CUDA events recorded around the launch on
+    its stream (sfft_execute_sync); for host input, the whole native host
+    pipeline -- H2D copies, kernels and D2H copies -- as the reference's
+    compute phase covers everything after the permute.
     """
-    if _is_torch(signal) and signal.is_cuda:
-        return TimedExecution(*_execute_device(plan, signal, timed=True))
-    t0 = time.perf_counter_ns()
-    host = signal.numpy() if _is_torch(signal) else signal
-    x, xc, _, _ = _prepare_host(plan, host)
-    dev = _default_device(plan)
-    xd = torch.from_numpy(xc).to(f"cuda:{dev}")
-    t_h2d = time.perf_counter_ns()
-    out_d, dispatch_us, compute_us = _execute_device(plan, xd, timed=True)
-    out = out_d.cpu().numpy()
     if _is_torch(signal):
-        out = torch.from_numpy(out)
-    return TimedExecution(out, (t_h2d - t0) / 1000.0 + dispatch_us, compute_us)
+        if signal.is_cuda:
+            return TimedExecution(*_execute_device(plan, signal, timed=True))
+        out, dispatch_us, compute_us = _execute_host(plan, signal.numpy(), timed=True)
+        return TimedExecution(torch.from_numpy(out), dispatch_us, compute_us)
+    return TimedExecution(*_execute_host(plan, signal, timed=True))

@@ -1,0 +1,58 @@
+"""Run the reference's own test suite (pkg/tests, 285 tests) against this package.
+
+``stagefft`` and its submodules are aliased to ``paper_2203_09384_b200`` so
+the reference's tests import this package unchanged; every test here is
+marked ``gpu`` because ``execute`` has no CPU fallback.  The suite itself is
+materialised by ``materialize.py`` (git-ignored copy of the reference files).
+
+``DEVIATIONS`` lists every reference test this package fails on purpose, with
+the reason; each is marked ``xfail(strict=True)``, so a deviation that stops
+failing -- or an unlisted failure -- turns the run red.  The list is the one
+in INTEGRATION.md section 4.
+"""
+
+from __future__ import annotations
+
+import importlib
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PKG = "paper_2203_09384_b200"
+SUBMODULES = ("bench", "cli", "errors", "estimator", "executor", "kernels", "numerics", "oracle", "planner",
+              "sigio", "signalgen", "stats", "validation")
+
+_pkg = importlib.import_module(PKG)
+sys.modules["stagefft"] = _pkg
+for _name in SUBMODULES:
+    sys.modules[f"stagefft.{_name}"] = importlib.import_module(f"{PKG}.{_name}")
+
+_N24 = "N = 2 and 4 are supported lengths here (north star: N = 2^1..2^11); the reference engine starts at 8"
+
+#: test node id (file::test[param]) -> reason.  Keep in sync with INTEGRATION.md section 4.
+DEVIATIONS: dict[str, str] = {
+    "test_ref_planner.py::test_factorization_rejects_out_of_range_powers": _N24,
+    "test_ref_planner.py::test_supported_lengths_constant": _N24,
+    "test_ref_planner.py::test_make_plan_rejects_unsupported_lengths": _N24,
+    "test_ref_estimator.py::test_unsupported_width_raises": _N24,
+    "test_ref_cli.py::test_bench_unsupported_length_still_runs_rest": _N24 + " (so `bench --lengths 4,8` runs both)",
+    "test_ref_estimator.py::test_get_params_and_clone":
+        "FourierTransformer has a third constructor parameter, precision='single' (double-precision plans)",
+}
+
+
+def pytest_collection_modifyitems(config, items):
+    here = os.path.dirname(os.path.abspath(__file__))
+    for item in items:
+        if not str(item.fspath).startswith(here):
+            continue
+        item.add_marker(pytest.mark.gpu)
+        key = f"{os.path.basename(str(item.fspath))}::{item.name}"
+        reason = DEVIATIONS.get(key)
+        if reason is not None:
+            item.add_marker(pytest.mark.xfail(reason=reason, strict=True))

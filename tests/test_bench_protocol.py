@@ -10,7 +10,7 @@ import json
 import pytest
 
 from paper_2203_09384_b200 import DomainError, InsufficientDataError
-from paper_2203_09384_b200.protocol import (
+from paper_2203_09384_b200.bench import (
     RECORD_COLUMNS,
     BenchmarkRecord,
     export_records,

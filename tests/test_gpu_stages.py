@@ -23,7 +23,7 @@ def run_pipeline(x, stages, direction="forward", precision="single"):
     table = sf.build_twiddle_table(n, precision)
     buf = sf.StageBuffer(sf.digit_reverse(x, stages, precision), 1)
     for i, r in enumerate(stages):
-        buf = sf.stages.RADIX_STAGE[r](buf, table, i, direction)
+        buf = sf.kernels.RADIX_STAGE[r](buf, table, i, direction)
     out = buf.data
     return out / n if direction == "inverse" else out
 

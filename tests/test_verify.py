@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from paper_2203_09384_b200 import DomainError, InsufficientDataError, ShapeError
-from paper_2203_09384_b200.verify import (
+from paper_2203_09384_b200.stats import (
     Histogram,
     build_histograms,
     chi2_p_value,
@@ -101,17 +101,22 @@ def test_compare_spectra_fields_and_detection():
 def test_naive_dft_matches_oracle(cuda):
     import oracle
     import paper_2203_09384_b200 as sf
-    from paper_2203_09384_b200.verify import naive_dft
+    from paper_2203_09384_b200.oracle import naive_dft, naive_dft_batch
 
     for n in (1, 5, 16, 100, 2048):
         x = oracle.generate_batch(3, n, seed=n, dtype=np.complex128)
         for d in ("forward", "inverse"):
-            got = naive_dft(x, d, precision="double")
+            got = naive_dft_batch(x, d, precision="double")
             want = oracle.direct_dft(x, d)
             assert np.max(np.abs(got - want)) <= 1e-9 * max(1.0, np.abs(want).max())
     assert naive_dft(np.arange(8.0)).dtype == np.complex64
     with pytest.raises(DomainError):
         naive_dft(np.array([1.0, np.nan]))
+    with pytest.raises(ShapeError):  # 1-D only, as the reference (tests/test_oracle.py)
+        naive_dft(np.ones((4, 4)))
+    # single-precision 1-D route == the batch route's single rounding
+    x = oracle.generate_batch(1, 64, seed=3, dtype=np.complex64)
+    assert np.array_equal(naive_dft(x[0]), naive_dft_batch(x)[0])
     assert sf is not None
 
 
@@ -119,7 +124,7 @@ def test_naive_dft_matches_oracle(cuda):
 def test_acceptance_criteria_2_3_on_gpu(cuda):
     """Reference acceptance criteria 2/3 (test_acceptance.py:94-114): ramp-2048."""
     import paper_2203_09384_b200 as sf
-    from paper_2203_09384_b200.verify import naive_dft
+    from paper_2203_09384_b200.oracle import naive_dft
 
     x = sf.generate("ramp", 2048)
     engine = sf.execute(sf.make_plan(2048), x)
@@ -135,12 +140,37 @@ def test_verify_batch_full_config(cuda, prec):
     import torch
 
     import paper_2203_09384_b200 as sf
-    from paper_2203_09384_b200.verify import naive_dft, verify_batch
+    from paper_2203_09384_b200.oracle import naive_dft_batch
+    from paper_2203_09384_b200.stats import verify_batch
 
     n, b = 1024, 4096
     x = torch.from_numpy(sf.generate_batch(b, n, seed=9, precision=prec)).to(cuda)
     y = sf.execute(sf.make_plan(n, precision=prec), x)
-    rep = verify_batch(y, naive_dft(x, precision="double"))
+    ref = naive_dft_batch(x, precision="double")
+    rep = verify_batch(y, ref)
     assert rep.rows == b
     assert rep.max_rel_l2 <= (1e-5 if prec == "single" else 1e-13) * 10
     assert rep.p_value_min >= 0.999
+    for bin_on in ("real", "imag"):
+        assert verify_batch(y, ref, bin_on=bin_on).p_value_min >= 0.999
+
+
+@pytest.mark.gpu
+def test_verify_batch_reports_true_minimum_p(cuda):
+    """p_value_min is the minimum over rows, not the p of the
+    largest reduced chi-square (rows differ in ndf)."""
+    import torch
+
+    from paper_2203_09384_b200.stats import verify_batch
+
+    rng = np.random.default_rng(4)
+    ref = torch.from_numpy(rng.standard_normal((6, 256)) + 1j * rng.standard_normal((6, 256)))
+    out = ref.clone()
+    out[2] *= 1.3  # one visibly different row
+    out[5, :128] *= 1.05
+    rep = verify_batch(out, ref)
+    ps = [verify_batch(out[i:i + 1], ref[i:i + 1]).p_value_min for i in range(6)]
+    assert rep.p_value_min == pytest.approx(min(ps), rel=1e-12, abs=1e-300)
+    assert rep.worst_row == int(np.argmin(ps))
+    with pytest.raises(ValueError):
+        verify_batch(out, ref, bin_on="phase")
