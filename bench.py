@@ -17,8 +17,16 @@ device time is the max over ranks (one all_reduce of a scalar).
 * ``roofline``  -- the FFT kernel vs the measured HBM copy bandwidth; the
                    average launch duration comes from a second pass of K
                    launches, each bracketed by its own events.
+* ``sweep``     -- BASELINE configs[2]: N = 2..2048 x {fp32, fp64}, forward,
+                   1 GiB input per launch, 20 timed launches per point, GB/s,
+                   roofline fraction, spot parity and clocks per point (N=1 only).
+* ``c4``        -- BASELINE configs[3]: fp64 N=2048, batch 131072 (4 GiB in),
+                   with its own roofline and clocks (N=1 only).
 * ``cpu_baseline`` -- the reference algorithm (oracle/, the batched restatement
-                   of stagefft) on all host cores, bounded sample, rank 0.
+                   of stagefft, bit-exact to it) on the host after all GPU
+                   timing, rank 0, every N: all cores (headline), one process,
+                   and the per-row loop the reference dispatches; CPU model and
+                   core count stated.
 
 ``--impl reference`` times only the reference CPU path (oracle port, all host
 cores) on the same config and prints the same line shape.
@@ -200,38 +208,62 @@ def host_link_rates(dev, nbytes=256 << 20, reps=3):
 
 # -------------------------------------------------------------- CPU baseline
 def _cpu_worker(args):
-    """Transform one resident chunk of rows ``reps`` times; returns (seconds, rows)."""
-    n, chunk_rows, reps, precision, direction, seed = args
+    """Transform one resident chunk of rows ``reps`` times; returns (seconds, rows).
+
+    ``per_row``: call the port one row at a time, as the reference's
+    FourierTransformer dispatches (estimator.py:61-68: one execute per row)."""
+    n, chunk_rows, reps, precision, direction, seed, per_row = args
     import oracle
 
     dtype = np.complex64 if precision == "single" else np.complex128
     x = oracle.generate_batch(chunk_rows, n, seed, dtype)
     t0 = time.perf_counter()
     for _ in range(reps):
-        oracle.reference_execute(x, direction, dtype=dtype)
+        if per_row:
+            for i in range(chunk_rows):
+                oracle.reference_execute(x[i:i + 1], direction, dtype=dtype)
+        else:
+            oracle.reference_execute(x, direction, dtype=dtype)
     return time.perf_counter() - t0, chunk_rows * reps
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 class CpuReference:
-    """The reference algorithm (oracle port) on all host cores.
+    """The reference algorithm (oracle port) on the host cores.
 
     One process per core (threads are useless under the GIL, BASELINE.md
     section 2), each transforming its own chunk of Philox rows (<= 8 MiB, so
-    memory stays bounded); rate = total rows / slowest worker.
+    memory stays bounded); rate = total rows / slowest worker.  ``per_row``
+    calls the port one row at a time (the reference's dispatch pattern);
+    ``procs=1`` is the single-process number.
     """
 
-    def __init__(self, n, precision, direction, procs=None):
+    def __init__(self, n, precision, direction, procs=None, per_row=False):
         import multiprocessing as mp
 
-        self.n, self.precision, self.direction = n, precision, direction
+        self.n, self.precision, self.direction, self.per_row = n, precision, direction, per_row
         self.procs = procs or os.cpu_count() or 1
-        self.chunk = max(1, min((8 << 20) // row_bytes(n, precision), 1 << 16))
+        cap = 256 if per_row else 1 << 16
+        self.chunk = max(1, min((8 << 20) // row_bytes(n, precision), cap))
         self.pool = mp.get_context("spawn").Pool(self.procs)
         res = self._map(1)  # warm imports, calibrate
         self.sec_per_rep = max(t for t, _ in res)
 
     def _map(self, reps):
-        args = [(self.n, self.chunk, reps, self.precision, self.direction, i) for i in range(self.procs)]
+        args = [(self.n, self.chunk, reps, self.precision, self.direction, i, self.per_row)
+                for i in range(self.procs)]
         return self.pool.map(_cpu_worker, args)
 
     def rate(self, target_s):
@@ -239,13 +271,145 @@ class CpuReference:
         res = self._map(reps)
         wall = max(t for t, _ in res)
         total = sum(r for _, r in res)
-        sample = (f"{self.procs} processes x {reps} x {self.chunk} Philox rows "
-                  f"(N={self.n}, {self.precision}, {self.direction}) in {wall:.1f}s")
+        mode = "one row per call" if self.per_row else "batched"
+        sample = (f"{self.procs} process(es) x {reps} x {self.chunk} Philox rows "
+                  f"(N={self.n}, {self.precision}, {self.direction}, {mode}) in {wall:.1f}s")
         return total / wall, self.procs, sample
 
     def close(self):
         self.pool.close()
         self.pool.join()
+
+
+def cpu_baseline(n, precision, direction, seconds):
+    """The reference algorithm on the host: all cores (the headline, batched
+    port), one process, and the per-row loop the reference dispatches
+    (single process and all cores).  Rates in rows/s -> GFLOP/s."""
+    fl = flops_per_row(n)
+    legs = {}
+    for key, procs, per_row, secs in (("all_cores", None, False, seconds),
+                                      ("single_process", 1, False, seconds / 3),
+                                      ("per_row_loop", 1, True, seconds / 3),
+                                      ("per_row_loop_all_cores", None, True, seconds / 3)):
+        cpu = CpuReference(n, precision, direction, procs=procs, per_row=per_row)
+        rate, cores, sample = cpu.rate(secs)
+        cpu.close()
+        legs[key] = {"value": round(rate * fl / 1e9, 4), "rows_per_s": round(rate, 1), "cores": cores,
+                     "sample": sample}
+    top = legs["all_cores"]
+    return {"value": top["value"], "unit": UNIT, "cores": top["cores"], "kind": "port",
+            "sample": top["sample"], "rows_per_s": top["rows_per_s"], "cpu_model": cpu_model(),
+            "host_cores": os.cpu_count(), **legs,
+            "note": "kind=port: the reference algorithm restated batched in numpy (oracle/stagefft_port.py, "
+                    "bit-exact to the reference); the reference itself is pure Python and cannot travel to "
+                    "the GPU box.  per_row_loop* call it one row at a time, the reference's dispatch."}
+
+
+# ------------------------------------------------- configs[2] and configs[3]
+def _timed_launches(sf, plan, x, y, rows, stream, launches, warmup):
+    """Mean ms per launch of `launches` back-to-back launches (two events on the
+    launch stream), after `warmup` untimed ones; host window for the clocks."""
+    import torch
+
+    for _ in range(warmup):
+        sf.launch(plan, x, y, rows, stream=stream)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a.record(stream)
+    for _ in range(launches):
+        sf.launch(plan, x, y, rows, stream=stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / launches, t0, time.perf_counter()
+
+
+def _spot_check(x, y, direction, rows):
+    """max rel-L2 of `rows` spread rows (first, last, CTA-boundary-ish) vs numpy complex128."""
+    b = x.shape[0]
+    idx = sorted({0, 1, b // 3, b // 2 - 1, b // 2, b - 2, b - 1} | set(range(0, b, max(1, b // rows))))[:rows + 7]
+    xi = x[idx].cpu().numpy().astype(np.complex128)
+    want = np.fft.fft(xi, axis=1) if direction == "forward" else np.fft.ifft(xi, axis=1)
+    got = y[idx].cpu().numpy()
+    return float(np.max(np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)))
+
+
+def _clock_brief(info):
+    return {"sm_mhz": info.get("sm_mhz"), "reasons": info.get("reasons", []), "power_w": info.get("power_w")}
+
+
+def run_sweep(sf, dev, stream, clocks, peak, launches=20, warmup=3, in_bytes=1 << 30, cool=0.3):
+    """BASELINE configs[2]: every N = 2..2048 in fp32 and fp64, forward, on a
+    fixed 1 GiB input (+ 1 GiB output), `launches` timed launches per point,
+    after `cool` idle seconds (the clocks recover between points)."""
+    import torch
+
+    buf_in = torch.empty(in_bytes, dtype=torch.uint8, device=dev)
+    buf_out = torch.empty(in_bytes, dtype=torch.uint8, device=dev)
+    points = []
+    t_start = time.perf_counter()
+    for precision in ("single", "double"):
+        real_t, cdt = ((torch.float32, torch.complex64) if precision == "single"
+                       else (torch.float64, torch.complex128))
+        buf_in.view(real_t).uniform_(-1.0, 1.0)
+        for p in range(1, 12):
+            n = 1 << p
+            rb = row_bytes(n, precision)
+            rows = in_bytes // rb
+            x = buf_in.view(cdt).view(rows, n)
+            y = buf_out.view(cdt).view(rows, n)
+            plan = sf.make_plan(n, "forward", precision=precision)
+            sf.launch(plan, x, y, rows, stream=stream)
+            torch.cuda.synchronize()
+            time.sleep(cool)
+            ms, t0, t1 = _timed_launches(sf, plan, x, y, rows, stream, launches, warmup)
+            gbs = 2 * rows * rb / (ms * 1e-3) / 1e9
+            points.append({
+                "precision": precision, "n": n, "batch": rows, "ms_per_launch": round(ms, 4),
+                "gbs": round(gbs, 1), "frac": round(gbs / peak, 4), "frac_of_8TBps_spec": round(gbs / 8000.0, 4),
+                "gflops": round(rows * flops_per_row(n) / (ms * 1e-3) / 1e9, 1),
+                "parity_rel_l2_max_vs_numpy_c128": _spot_check(x, y, "forward", 16),
+                "clocks": _clock_brief(clocks.summary(t0, t1)),
+            })
+    del buf_in, buf_out
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE configs[2]: N=2^1..2^11, fp32 and fp64, forward, 1 GiB input + 1 GiB output "
+                        "per launch (> 126 MB L2), device-resident uniform rows",
+            "launches_per_point": launches, "warmup_per_point": warmup, "cool_s": cool, "peak_gbs": peak,
+            "wall_s": round(time.perf_counter() - t_start, 1), "points": points,
+            "min_frac": min(pt["frac"] for pt in points)}
+
+
+def run_c4(sf, dev, stream, clocks, peak, launches=20, warmup=3, cool=0.3):
+    """BASELINE configs[3]: fp64 forward N=2048, B=131072 (4 GiB in + 4 GiB out)."""
+    import torch
+
+    n, rows = 2048, 131072
+    rb = row_bytes(n, "double")
+    x = torch.empty((rows, n), dtype=torch.complex128, device=dev)
+    torch.view_as_real(x).uniform_(-1.0, 1.0)
+    y = torch.empty_like(x)
+    plan = sf.make_plan(n, "forward", precision="double")
+    sf.launch(plan, x, y, rows, stream=stream)
+    torch.cuda.synchronize()
+    time.sleep(cool)
+    ms, t0, t1 = _timed_launches(sf, plan, x, y, rows, stream, launches, warmup)
+    gbs = 2 * rows * rb / (ms * 1e-3) / 1e9
+    parity = _spot_check(x, y, "forward", 32)
+    info = plan.kernel_info(dev.index or 0)
+    del x, y
+    torch.cuda.empty_cache()
+    return {"workload": "fp64 forward C2C FFT N=2048 batch=131072 (BASELINE configs[3]; 4 GiB in + 4 GiB out)",
+            "value": round(rows * flops_per_row(n) / (ms * 1e-3) / 1e9, 1), "unit": UNIT,
+            "ms_per_launch": round(ms, 4), "launches": launches,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "frac_of_8TBps_spec": round(gbs / 8000.0, 4),
+                         "algorithmic_bytes_per_launch": 2 * rows * rb,
+                         "traffic": ncu_traffic(CONFIGS["c4"][4]), "traffic_source": "profiles/ncu_summary.json (ncu --set full)"},
+            "kernel": {k: info[k] for k in ("kernel", "elems_per_thread", "seqs_per_cta", "threads_per_cta",
+                                            "radices", "loader", "variant")},
+            "parity_rel_l2_max_vs_numpy_c128": parity,
+            "clocks": _clock_brief(clocks.summary(t0, t1))}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -363,7 +527,6 @@ def run_gpu(args, n, batch, precision, direction, workload):
     for _ in range(e2e_steps):
         sf.execute(plan, hin_np, out=hout_np)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
-    clocks.stop()
     if rank == 0 and not args.no_check:
         assert np.array_equal(hout_np[:64], y[:64].cpu().numpy()), "e2e output differs from device output"
 
@@ -376,6 +539,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
     value = total_rows * fl / (region_ms / args.steps * 1e-3) / 1e9
     e2e_value = e2e_rows * fl / e2e_s / 1e9
     peak, peak_src = hbm_peak()
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     achieved = batch * 2 * rb / (kernel_ms * 1e-3) / 1e9
     info = plan.kernel_info(local)
     out = {
@@ -399,7 +563,10 @@ def run_gpu(args, n, batch, precision, direction, workload):
             "precision": precision,
             "direction": direction,
             "parallelism": f"batch-sharded x{world} (independent launches, no collective)",
-            "l2_policy": f"input {batch * rb / 2**20:.0f} MiB per GPU > 126 MB L2; no flush needed",
+            "l2_policy": (f"input {batch * rb / 2**20:.0f} MiB per GPU > {l2_bytes / 2**20:.0f} MiB L2; no flush needed"
+                          if batch * rb > l2_bytes else
+                          f"input {batch * rb / 2**20:.0f} MiB per GPU fits the {l2_bytes / 2**20:.0f} MiB L2 "
+                          "(small test config; not a bench number)"),
             "kernel": {k: info[k] for k in ("kernel", "elems_per_thread", "seqs_per_cta", "threads_per_cta", "radices", "variant")},
         },
         "e2e": {
@@ -436,14 +603,17 @@ def run_gpu(args, n, batch, precision, direction, workload):
         "clocks": clock_info,
         "parity_rel_l2_max_first64_vs_numpy_c128": parity,
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = CpuReference(n, precision, direction)
-        rate, cores, sample = cpu.rate(args.cpu_seconds)
-        cpu.close()
-        out["cpu_baseline"] = {"value": round(rate * fl / 1e9, 4), "unit": UNIT, "cores": cores,
-                               "kind": "port", "sample": sample,
-                               "rows_per_s": round(rate, 1)}
+    if world == 1 and not args.no_extras:
+        # BASELINE configs[2] and [3] under the same clock record as `value`
+        out["sweep"] = run_sweep(sf, dev, stream, clocks, peak)
+        out["c4"] = run_c4(sf, dev, stream, clocks, peak)
+    clocks.stop()
+    barrier()  # every rank's GPU work is done before rank 0 loads the host
+    if rank == 0 and not args.no_cpu:
+        # rank 0 only, outside every timed region (the other ranks wait below)
+        out["cpu_baseline"] = cpu_baseline(n, precision, direction, args.cpu_seconds)
     if world > 1:
+        barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -511,10 +681,12 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the sweep (configs[2]) and c4 (configs[3]) keys")
     ap.add_argument("--fill-hbm", type=float, default=0.0, metavar="FRAC",
                     help="size the batch so input + output take FRAC of free HBM (BASELINE configs[3]); "
                          "the e2e leg then runs on a <= 4 GiB host block")
-    args = ap.parse_args()
+    argv = json.loads(os.environ["SFFT_BENCH_ARGV"]) if "SFFT_BENCH_ARGV" in os.environ else None
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -525,8 +697,11 @@ def main():
         sock.bind(("127.0.0.1", 0))
         port = sock.getsockname()[1]
         sock.close()
+        # our arguments travel in the environment: torchrun's own parser would
+        # otherwise claim abbreviations such as --n (--nnodes / --nproc-per-node)
+        os.environ["SFFT_BENCH_ARGV"] = json.dumps(sys.argv[1:])
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
         os.execv(sys.executable, cmd)
     n, batch, precision, direction, workload = CONFIGS[args.config]
     if any(v is not None for v in (args.n, args.batch, args.precision, args.direction)):

@@ -53,7 +53,7 @@ def test_warmup_below_three_is_rejected():
 @pytest.mark.gpu
 def test_gpu_arm_line(cuda):
     lines = run_bench(["--n", "256", "--batch", "65536", "--steps", "5", "--warmup", "3", "--no-cpu",
-                       "--e2e-steps", "1"])
+                       "--e2e-steps", "1"], timeout=900)
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 5 and d["scaling"] == "weak"
@@ -65,3 +65,36 @@ def test_gpu_arm_line(cuda):
     assert d["gpu_launches"] == 5
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["parity_rel_l2_max_first64_vs_numpy_c128"] < 1e-5 * 8
+    # BASELINE configs[2] (sweep) and configs[3] (c4) ride on the same line
+    sweep = d["sweep"]
+    assert [(p["precision"], p["n"]) for p in sweep["points"]] == [
+        (prec, 2**k) for prec in ("single", "double") for k in range(1, 12)]
+    for p in sweep["points"]:
+        assert p["batch"] * p["n"] * (8 if p["precision"] == "single" else 16) == 1 << 30
+        assert p["gbs"] > 0 and abs(p["frac"] - p["gbs"] / sweep["peak_gbs"]) < 1e-3
+        tol = (1e-5 if p["precision"] == "single" else 1e-13) * (p["n"].bit_length() - 1)
+        assert p["parity_rel_l2_max_vs_numpy_c128"] <= tol
+        assert "sm_mhz" in p["clocks"]
+    c4 = d["c4"]
+    assert c4["roofline"]["algorithmic_bytes_per_launch"] == 2 * 131072 * 2048 * 16
+    assert c4["parity_rel_l2_max_vs_numpy_c128"] <= 1e-13 * 11 and c4["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_with_cpu_baseline(cuda):
+    """bench.py --gpus 2 under torchrun: two ranks share the one GPU of the
+    test box through the SFFT_BENCH_DEVICE / gloo hooks.  Checks the
+    whole-job accounting and that rank 0 adds the CPU baseline at N > 1."""
+    lines = run_bench(["--gpus", "2", "--n", "128", "--batch", "32768", "--steps", "4", "--warmup", "3",
+                       "--e2e-steps", "1", "--cpu-seconds", "1.5"],
+                      {"SFFT_BENCH_DEVICE": "0", "SFFT_BENCH_DIST_BACKEND": "gloo"}, timeout=900)
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 * 32768 and d["scaling"] == "weak"
+    assert d["config"]["batch_per_gpu"] == 32768
+    cpu = d["cpu_baseline"]
+    assert cpu["kind"] == "port" and cpu["cores"] >= 1 and cpu["value"] > 0
+    for leg in ("all_cores", "single_process", "per_row_loop", "per_row_loop_all_cores"):
+        assert cpu[leg]["value"] > 0 and cpu[leg]["cores"] >= 1
+    assert cpu["single_process"]["cores"] == 1 and cpu["per_row_loop"]["cores"] == 1
+    assert "sweep" not in d  # the configs[2]/[3] keys are single-GPU lines only
