@@ -21,6 +21,7 @@ from .stagefft_port import (  # noqa: F401
     factorize_stages,
     generate,
     generate_batch,
+    generate_rows,
     mixed_radix_execute,
     reference_execute,
     split_radix_execute,

@@ -305,3 +305,32 @@ def generate_batch(batch: int, n: int, seed: int = 0, dtype=np.complex64) -> np.
     rng = np.random.Generator(np.random.Philox(key=seed))
     parts = rng.uniform(-1.0, 1.0, size=(2, batch, n))
     return (parts[0] + 1j * parts[1]).astype(dtype)
+
+
+def _philox_draws(seed: int, start: int, count: int) -> np.ndarray:
+    """``count`` uniform(-1, 1) draws of ``Generator(Philox(key=seed))`` starting
+    at flat draw index ``start``, without generating the ones before it.
+
+    One Philox counter step yields 4 64-bit draws and ``advance(k)`` skips k
+    steps; ``uniform`` consumes exactly one draw per double.
+    """
+    bg = np.random.Philox(key=seed)
+    bg.advance(start // 4)
+    rng = np.random.Generator(bg)
+    skip = start % 4
+    return rng.uniform(-1.0, 1.0, size=skip + count)[skip:]
+
+
+def generate_rows(batch: int, n: int, rows, seed: int = 0, dtype=np.complex64) -> np.ndarray:
+    """Rows ``rows`` of ``generate_batch(batch, n, seed, dtype)``, bit for bit,
+    at a cost proportional to ``len(rows)`` -- for sampled checks of
+    multi-GiB batches.  Real parts are draws [r*n, (r+1)*n) of the (2, B, N)
+    stream, imaginary parts the same range offset by B*n."""
+    rows = np.asarray(rows, dtype=np.int64)
+    out = np.empty((rows.size, n), dtype=dtype)
+    for i, r in enumerate(rows):
+        re = _philox_draws(seed, int(r) * n, n)
+        im = _philox_draws(seed, (batch + int(r)) * n, n)
+        out[i] = (re + 1j * im).astype(dtype)
+    return out
+

@@ -54,7 +54,7 @@ def test_random_shapes_match_oracle(cuda, c):
     exact = oracle.direct_dft(sub, c["direction"])
     tol = tolerance(n, prec)
     assert row_rel_l2(got, exact).max() <= tol
-    assert row_rel_l2(got, want).max() <= 2 * tol
+    assert row_rel_l2(got, want).max() <= tol
 
 
 @settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])

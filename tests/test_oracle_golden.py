@@ -118,3 +118,13 @@ def test_round_trip_parseval_linearity():
     a, b = 2.5 - 0.5j, -1.25 + 3.0j
     lhs = oracle.reference_execute(a * x + b * y, "forward", dtype=np.complex128)
     assert rel_l2(lhs, a * fx + b * oracle.reference_execute(y, "forward", dtype=np.complex128)) <= 1e-14
+
+
+def test_generate_rows_matches_generate_batch():
+    """oracle.generate_rows (Philox jump-ahead) reproduces sampled rows of a
+    batch bit for bit -- the sampled config-shape parity tests rely on it."""
+    for batch, n, seed, dt in [(7, 8, 3, np.complex64), (33, 2, 0, np.complex128), (5, 2048, 9, np.complex64),
+                               (1000, 4, 2, np.complex128)]:
+        full = oracle.generate_batch(batch, n, seed, dt)
+        idx = [0, batch - 1, batch // 2, 1, batch // 3]
+        assert np.array_equal(oracle.generate_rows(batch, n, idx, seed, dt), full[idx])
