@@ -4,7 +4,7 @@
 // Replaces the per-stage numpy arithmetic of the reference butterfly engine:
 //   kernels.py:98-104  (_dft4: radix-4 DFT with rot = -i)
 //   kernels.py:126-151 (radix8_stage: two DFT-4s + eighth-root constants)
-// Here a radix-r DFT (r <= 32) is a radix-2 decision-in-frequency network over
+// Here a radix-r DFT (r <= 64) is a radix-2 decision-in-frequency network over
 // r registers; every twiddle inside it is a compile-time constant, and the
 // +-1, +-i and (+-1 +- i)/sqrt(2) factors are strength-reduced exactly like the
 // reference's radix-8 constants (kernels.py:136-141).  Only forward kernels
@@ -42,27 +42,36 @@ __host__ __device__ constexpr int bitrev(int k, int bits) {
   return r;
 }
 
-// cos(2*pi*j/32), j in [0, 32), correctly rounded doubles (50-digit reference).
-__host__ __device__ constexpr double cos32(int j) {
-  j &= 31;
-  if (j > 16) j = 32 - j;  // cos is even
+// cos(2*pi*j/64), j in [0, 64), correctly rounded doubles (50-digit mpmath
+// reference, rounded once).  Radix-r DFTs use the r-th roots, r <= 64.
+__host__ __device__ constexpr double cos64(int j) {
+  j &= 63;
+  if (j > 32) j = 64 - j;  // cos is even
   bool neg = false;
-  if (j > 8) { j = 16 - j; neg = true; }  // cos(pi - x) = -cos(x)
+  if (j > 16) { j = 32 - j; neg = true; }  // cos(pi - x) = -cos(x)
   double c = 0.0;
   switch (j) {
     case 0: c = 1.0; break;
-    case 1: c = 0.9807852804032304; break;
-    case 2: c = 0.9238795325112867; break;
-    case 3: c = 0.8314696123025452; break;
-    case 4: c = 0.7071067811865476; break;
-    case 5: c = 0.5555702330196022; break;
-    case 6: c = 0.3826834323650898; break;
-    case 7: c = 0.19509032201612828; break;
+    case 1: c = 0.9951847266721969; break;
+    case 2: c = 0.9807852804032304; break;
+    case 3: c = 0.9569403357322088; break;
+    case 4: c = 0.9238795325112867; break;
+    case 5: c = 0.881921264348355; break;
+    case 6: c = 0.8314696123025452; break;
+    case 7: c = 0.773010453362737; break;
+    case 8: c = 0.7071067811865476; break;
+    case 9: c = 0.6343932841636455; break;
+    case 10: c = 0.5555702330196022; break;
+    case 11: c = 0.47139673682599764; break;
+    case 12: c = 0.3826834323650898; break;
+    case 13: c = 0.2902846772544624; break;
+    case 14: c = 0.19509032201612828; break;
+    case 15: c = 0.0980171403295606; break;
     default: c = 0.0; break;
   }
   return neg ? -c : c;
 }
-__host__ __device__ constexpr double sin32(int j) { return cos32(8 - j + 32); }
+__host__ __device__ constexpr double sin64(int j) { return cos64(16 - j + 64); }
 
 // ------------------------------------------------------------ complex helpers
 // fp64: scalar DADD/DFMA.  fp32: Blackwell's packed FP32x2 pipe (FADD2 /
@@ -106,7 +115,7 @@ template <typename C> __device__ __forceinline__ C cswap(C a) { return C{a.y, a.
 template <typename C> __device__ __forceinline__ C mul_minus_i(C a) { return C{a.y, -a.x}; }
 template <typename C> __device__ __forceinline__ C mul_plus_i(C a) { return C{-a.y, a.x}; }
 
-// a * exp(-2*pi*i*J/L) with J, L compile-time, L a power of two <= 32.
+// a * exp(-2*pi*i*J/L) with J, L compile-time, L a power of two <= 64.
 template <int J, int L, typename C>
 __device__ __forceinline__ C twiddle_const(C a) {
   using T = decltype(a.x);
@@ -131,9 +140,9 @@ __device__ __forceinline__ C twiddle_const(C a) {
     } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
       return mul2(add2(a, mul_plus_i(a)), make_float2(h, h));
     } else {
-      constexpr int j32 = j * (32 / L);
-      constexpr T c = T(cos32(j32));
-      constexpr T s = T(-sin32(j32));
+      constexpr int j64 = j * (64 / L);
+      constexpr T c = T(cos64(j64));
+      constexpr T s = T(-sin64(j64));
       return fma2(make_float2(-a.y, a.x), make_float2(s, s), mul2(a, make_float2(c, c)));  // immediates
     }
   } else {
@@ -148,9 +157,9 @@ __device__ __forceinline__ C twiddle_const(C a) {
     } else if constexpr (8 * j == 7 * L) {  // (1 + i)/sqrt2
       return C{__dmul_rn(a.x - a.y, h), __dmul_rn(a.x + a.y, h)};
     } else {
-      constexpr int j32 = j * (32 / L);
-      constexpr T c = T(cos32(j32));
-      constexpr T s = T(-sin32(j32));
+      constexpr int j64 = j * (64 / L);
+      constexpr T c = T(cos64(j64));
+      constexpr T s = T(-sin64(j64));
       return cmul(a, C{c, s});
     }
   }
@@ -159,7 +168,7 @@ __device__ __forceinline__ C twiddle_const(C a) {
 // In-place forward DFT of R registers, natural order in and out.
 template <int R, typename C>
 __device__ __forceinline__ void dft_regs(C (&v)[R]) {
-  static_assert((R & (R - 1)) == 0 && R >= 1 && R <= 32, "radix");
+  static_assert((R & (R - 1)) == 0 && R >= 1 && R <= 64, "radix");
   if constexpr (R == 1) {
     return;
   } else {

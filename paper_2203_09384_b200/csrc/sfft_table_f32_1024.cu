@@ -19,6 +19,7 @@ std::vector<Variant> table_f32_1024(int log2n) {
           stockham_variant<float, 1024, 32, 4, 1, 1>(),
           pipe_variant<float, 1024, 16, 2, 1, 1, 3>(),
           stockham_variant<float, 1024, 32, 2, 1, 2, 0, true>(),
+          stockham_variant<float, 1024, 32, 4, 1, 1, 1>(),  // r02 study: R32 + bulk TMA, 4 sequences
       };
     default:
       return {};

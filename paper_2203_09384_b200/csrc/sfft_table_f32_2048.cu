@@ -9,18 +9,27 @@ std::vector<Variant> table_f32_2048(int log2n) {
   switch (log2n) {
     case 11:
       return {
-          // default: two-level twiddles (TWP 2) -- ramp-2048 |error| 0.072 against
-          // 0.129 for TWP 1, inside the reference's own 0.1 bound
-          // (tests/test_stats.py:211-222); burst equal, sustained -0.7 %
-          // (profiles/r02_twiddle_policy.txt)
-          stockham_variant<float, 2048, 16, 1, 1, 2, 0, true>(),
+          // default (round 2): one warp per sequence, R = 64, passes [64, 32]
+          // (one exchange, __syncwarp only), one bulk TMA copy per sequence,
+          // TWP 1.  Under sustained power-capped load it holds 6.49-6.85 TB/s
+          // where the round-1 R16 design held 6.09-6.57 (+4-7 %, >= 1.0x the
+          // copy's own sustained rate); real input 6.50 vs 6.08 TB/s; burst
+          // -1.2 % (profiles/r02_wide_radix_study.txt).  Ramp-2048 |error|
+          // 0.066 < 0.1, the reference's bound (tests/test_stats.py:211-222).
+          stockham_variant<float, 2048, 64, 1, 1, 1, 1, true>(),
+          stockham_variant<float, 2048, 16, 1, 1, 2>(),     // R16 TWP 2 LDG (round-2 interim default)
           stockham_variant<float, 2048, 16, 1, 1>(),
           stockham_variant<float, 2048, 16, 1, 2>(),
           stockham_variant<float, 2048, 32, 1, 1>(),
           stockham_variant<float, 2048, 16, 1, 1, 1, 1>(),
           stockham_variant<float, 2048, 32, 1, 1, 1>(),
           stockham_variant<float, 2048, 32, 2, 1, 1>(),
-          stockham_variant<float, 2048, 16, 1, 1, 1>(),  // round-1 default (TWP 1)
+          stockham_variant<float, 2048, 16, 1, 1, 1>(),     // round-1 default (R16 TWP 1 LDG)
+          stockham_variant<float, 2048, 16, 1, 1, 2, 1>(),  // R16 TWP 2 + bulk TMA
+          stockham_variant<float, 2048, 64, 1, 1, 1, 0>(),  // R64, LDG
+          stockham_variant<float, 2048, 64, 4, 1, 1, 0>(),  // R64, LDG, 4 sequences per CTA
+          stockham_variant<float, 2048, 64, 2, 1, 1, 1>(),  // R64, bulk TMA, 2 sequences per CTA
+          stockham_variant<float, 2048, 64, 1, 1, 2, 1>(),  // R64, TWP 2, bulk TMA (ramp |error| 0.128 > 0.1)
       };
     default:
       return {};

@@ -15,7 +15,14 @@ std::vector<Variant> table_f64_2048(int log2n) {
           stockham_variant<double, 2048, 16, 1, 1>(),
           stockham_variant<double, 2048, 16, 1, 2, 1>(),
           pipe_variant<double, 2048, 16, 1, 2, 1, 3>(),
-          stockham_variant<double, 2048, 16, 1, 2, 2, 1, true>(),
+          stockham_variant<double, 2048, 16, 1, 2, 2, 1>(),  // TWP 2 + bulk TMA
+          stockham_variant<double, 2048, 16, 1, 2, 0, 1>(),  // TWP 0 + bulk TMA
+          pipe_variant<double, 2048, 16, 1, 2, 1, 2>(),      // 2-stage pipeline (64 KB, 3 CTAs/SM)
+          // R32 (passes [32, 32, 2], two warps per sequence) + bulk TMA: +1.2 %
+          // sustained, -1.2 % burst, +5 % real input against entry 0 -- within
+          // box-to-box noise, so entry 0 stays (profiles/r02_wide_radix_study.txt)
+          stockham_variant<double, 2048, 32, 1, 2, 1, 1, true>(),
+          stockham_variant<double, 2048, 32, 1, 2, 1, 0>(),  // R32, LDG
       };
     default:
       return {};

@@ -249,3 +249,28 @@ def test_real_numpy_input_host_path(cuda, prec, pinned):
         assert got.dtype == plan.dtype and got.shape == x.shape
         assert np.array_equal(got, want)
     assert np.array_equal(sf.execute_sharded(plan, x, [0, 0]), want)
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_real_input_every_real_capable_variant(cuda, prec):
+    """Every compiled variant with a real-input loader (LDG or bulk TMA, any
+    R) is bit-identical to widening, on odd batches (partial CTAs)."""
+    lib = sf._native.lib()
+    code = 0 if prec == "single" else 1
+    rdt = torch.float32 if prec == "single" else torch.float64
+    cdt = torch.complex64 if prec == "single" else torch.complex128
+    checked = 0
+    for p in range(1, 12):
+        n = 2**p
+        for v in range(lib.sfft_num_variants(n, code)):
+            if not sf._native.variant_info(n, code, v)["real_input"]:
+                continue
+            xr = torch.rand((301, n), device=cuda, dtype=rdt) * 2 - 1
+            for direction in ("forward", "inverse"):
+                plan = sf.make_plan(n, direction, precision=prec, variant=v)
+                y = torch.empty((301, n), dtype=cdt, device=cuda)
+                sf.launch(plan, xr, y, 301)
+                torch.cuda.synchronize()
+                assert torch.equal(y, sf.execute(plan, xr.to(cdt))), (n, v, direction)
+                checked += 1
+    assert checked >= 2 * 11

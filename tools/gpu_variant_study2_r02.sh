@@ -1,0 +1,7 @@
+# Round-2 study 2: wide-radix variants (one warp per sequence, fewer passes) for fp32 N=2048, fp64 N=1024/2048.
+set -x
+python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "all_kernel_variants" 2>&1 | tail -2
+python tools/sweep.py --all-variants --cool 0.3 --n 1024,2048 --json gpurun_out/r02_sweep_study2.json > /dev/null 2>&1
+for spec in "2048 single 65536 copy,0,9,10,11,12" "1024 double 65536 copy,0,8,9,10" "2048 double 32768 copy,0,9,10" "1024 single 131072 copy,0,10"; do
+  python tools/sustained.py $spec --secs 4 --rounds 2 >> gpurun_out/r02_sustained_study2.jsonl 2>&1
+done

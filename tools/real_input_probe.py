@@ -29,13 +29,13 @@ for prec in ("single", "double"):
         rows = (1 << 30) // (n * 2 * resz)
         xr = torch.rand((rows, n), dtype=rdt, device="cuda")
         y = torch.empty((rows, n), dtype=cdt, device="cuda")
-        plan = sf.make_plan(n, precision=prec)
+        plan = sf.make_plan(n, precision=prec, variant=int(os.environ.get(f"VARIANT_{prec.upper()}_{n}", "0")))
         fused = lambda: sf.launch(plan, xr, y, rows)  # noqa: E731
         widen = lambda: sf.launch(plan, xr.to(cdt), y, rows)  # noqa: E731
         for f in (fused, widen):
             f()
         tf, tw = timed(fused), timed(widen)
-        print(json.dumps({"prec": prec, "n": n, "rows": rows, "fused_us": round(tf, 1), "widen_then_c2c_us": round(tw, 1),
+        print(json.dumps({"prec": prec, "n": n, "variant": plan.variant, "rows": rows, "fused_us": round(tf, 1), "widen_then_c2c_us": round(tw, 1),
                           "speedup": round(tw / tf, 2),
                           "fused_gbs": round(rows * n * 3 * resz / tf / 1e3, 1)}), flush=True)
         del xr, y
