@@ -311,7 +311,7 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
 
   // per-pass table: pass p >= 1, entry [(q-1)*L + k] = w_{L r}^{q k} = base[(n/(L r)) q k]
   std::vector<int> tidx;
-  if (p->v->kernel == SFFT_KERNEL_STOCKHAM) {
+  if (p->v->kernel != SFFT_KERNEL_TILE) {  // stockham and split2: per-pass tables
     int L = p->v->radices[0];
     for (int pass = 1; pass < p->v->passes; ++pass) {
       const int r = p->v->radices[pass];

@@ -419,6 +419,110 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
                                                   s, valid ? out + seq * N : nullptr, tw);
 }
 
+// Two-warp kernel for N = 2 * 32 * R (fp64 N = 2048 with R = 32): one level of
+// radix-2 decimation in time around two one-warp Stockham FFTs.
+//
+// A length-N transform with R elements per thread needs ceil(log_R N) passes,
+// i.e. three for fp64 N = 2048 at R <= 32 (R = 64 would need 256 registers
+// of data).  Here the CTA (64 threads) takes one sequence with one bulk TMA
+// copy; warp w transforms the w-th polyphase half h_w[i] = x[2i + w] (i < N/2)
+// with the two-pass, __syncwarp-only passes of the N/2 kernel in its own
+// exchange region; then the warps trade half their results through shared
+// memory (one 64-thread barrier) and finish with the radix-2 combine
+//   X[k] = E[k] + w_N^k O[k],   X[k + N/2] = E[k] - w_N^k O[k]
+// -- warp 0 for k < N/4, warp 1 for k >= N/4 -- storing coalesced rows.
+// Per element: 1.5 shared-memory exchanges instead of 2 and one CTA barrier
+// instead of four.  The gather of the polyphase halves from the linear TMA
+// staging reads every other 16-byte element (2-way bank conflict on that
+// one access; the exchanges stay conflict-free).
+// Twiddles: the N/2 transform's per-pass table, then w_N^k for k < N/2 --
+// exactly the generic per-pass table of the pass list [R, ..., 2].
+template <typename T, int N, int R, bool INV, int LAYOUT, int TWP, bool RIN = false>
+__global__ void __launch_bounds__(64)
+split2_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
+              const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  using S = Smem<T, LAYOUT, R>;
+  constexpr int H = N / 2;       // half length
+  constexpr int G = H / R;       // threads per half transform
+  constexpr int SH = S::size(H);  // exchange elements per warp
+  constexpr int HR = R / 2;
+  static_assert(G == 32, "one warp per half transform");
+  static_assert(2 * SH >= N, "staging fits the exchange regions");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  __shared__ __align__(8) unsigned long long bar;
+
+  const int tid = threadIdx.x;
+  const int w = tid >> 5;
+  const int j = tid & 31;
+  const long long seq = blockIdx.x;  // one sequence per CTA: every CTA is full
+  pdl_enter();
+
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    constexpr uint32_t bytes = uint32_t(N * int(sizeof(*in)));
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(sm, in + seq * N, bytes, &bar);
+  }
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+
+  // polyphase half w: v[m] = x[2 (j + m G) + w]
+  C v[R];
+  if constexpr (RIN) {
+    const T* smr = reinterpret_cast<const T*>(smem_raw);
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = C{smr[2 * (j + m * G) + w], T(0)};
+  } else {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = sm[2 * (j + m * G) + w];
+  }
+  __syncthreads();  // staging fully read before the exchange regions reuse it
+  if (nonfinite != nullptr) check_nonfinite<T, R>(v, nonfinite);
+  if constexpr (INV) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
+  }
+  // E (w = 0) or O (w = 1) in natural order: v[m] = F[j + m G]
+  stockham_passes<T, H, R, 1, false, LAYOUT, TWP>(v, sm + w * SH, 0, j, 0, nullptr, tw);
+
+  // trade halves: warp 0 keeps k < H/2 and needs O there; warp 1 keeps
+  // k >= H/2 and needs E there.  Linear [m][lane] slots: conflict-free.
+  __syncthreads();  // both warps done with their exchange regions
+  C* xs = sm;
+  if (w == 0) {
+#pragma unroll
+    for (int m = 0; m < HR; ++m) xs[(HR + m) * 32 + j] = v[HR + m];  // E, upper
+  } else {
+#pragma unroll
+    for (int m = 0; m < HR; ++m) xs[m * 32 + j] = v[m];  // O, lower
+  }
+  __syncthreads();
+  const C* twc = tw + twiddle_table_len(H, R);  // w_N^k, k < H
+  C* dst = out + seq * N;
+  constexpr T scale = T(1) / T(N);  // exact: N = 2^k
+  auto combine = [&](C e, C o, int k) {
+    const C t = cmul(o, __ldg(twc + k));
+    C y0 = cadd(e, t);
+    C y1 = csub(e, t);
+    if constexpr (INV) {
+      y0 = cscale(cswap(y0), scale);
+      y1 = cscale(cswap(y1), scale);
+    }
+    st_stream(dst + k, y0);
+    st_stream(dst + k + H, y1);
+  };
+  if (w == 0) {
+#pragma unroll
+    for (int m = 0; m < HR; ++m) combine(v[m], xs[m * 32 + j], j + m * G);
+  } else {
+#pragma unroll
+    for (int m = 0; m < HR; ++m) combine(xs[(HR + m) * 32 + j], v[HR + m], j + (HR + m) * G);
+  }
+}
+
 // Persistent, pipelined variant: a grid of (SMs x resident CTAs) walks the
 // batch in tiles of SEQ sequences (tile t, t + grid, ...).  Each CTA owns
 // STAGES shared-memory buffers; one thread keeps STAGES - 1 bulk TMA copies

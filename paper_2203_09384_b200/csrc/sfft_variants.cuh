@@ -222,6 +222,53 @@ Variant pipe_variant() {
   return v;
 }
 
+// two-warp split-radix-2 kernel (sfft_kernels.cuh: split2_kernel)
+template <typename T, int N, int R, int LAYOUT>
+constexpr int split2_smem() {
+  return 2 * sfft::Smem<T, LAYOUT, R>::size(N / 2) * int(sizeof(sfft::cx_t<T>));
+}
+template <typename T, int N, int R, bool INV, int LAYOUT, int TWP, bool RIN = false>
+cudaError_t launch_split2(const void* in, void* out, const void* tw, long long batch, int* flag,
+                          cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
+  return launch_pdl(pdl, sfft::split2_kernel<T, N, R, INV, LAYOUT, TWP, RIN>, batch, 64,
+                    split2_smem<T, N, R, LAYOUT>(), st, static_cast<const In*>(in), static_cast<C*>(out),
+                    static_cast<const C*>(tw), batch, flag);
+}
+template <typename T, int N, int R, bool INV, int LAYOUT, int TWP, bool RIN = false>
+cudaError_t prepare_split2(int carveout) {
+  const auto k = sfft::split2_kernel<T, N, R, INV, LAYOUT, TWP, RIN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, split2_smem<T, N, R, LAYOUT>());
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+// Pass list and twiddle table are the generic Stockham ones for (N, R) --
+// [R, ..., 2] with the radix-2 level last -- so only the launch changes.
+template <typename T, int N, int R, int LAYOUT, int TWP, bool REAL = false>
+Variant split2_variant() {
+  static_assert(sfft::pass_radix(N, R, sfft::num_passes(N, R) - 1) == 2 && N / 2 / R == 32, "split2 geometry");
+  Variant v = stockham_variant<T, N, R, 1, LAYOUT, TWP, 1>();
+  v.kernel = SFFT_KERNEL_SPLIT2;
+  v.threads = 64;
+  v.seq = 1;
+  v.smem = split2_smem<T, N, R, LAYOUT>();
+  v.carveout = -1;  // the bulk copy lands in shared memory
+  v.launch[0] = &launch_split2<T, N, R, false, LAYOUT, TWP>;
+  v.launch[1] = &launch_split2<T, N, R, true, LAYOUT, TWP>;
+  v.prepare[0] = &prepare_split2<T, N, R, false, LAYOUT, TWP>;
+  v.prepare[1] = &prepare_split2<T, N, R, true, LAYOUT, TWP>;
+  v.launch_real[0] = v.launch_real[1] = nullptr;
+  v.prepare_real[0] = v.prepare_real[1] = nullptr;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_split2<T, N, R, false, LAYOUT, TWP, true>;
+    v.launch_real[1] = &launch_split2<T, N, R, true, LAYOUT, TWP, true>;
+    v.prepare_real[0] = &prepare_split2<T, N, R, false, LAYOUT, TWP, true>;
+    v.prepare_real[1] = &prepare_split2<T, N, R, true, LAYOUT, TWP, true>;
+  }
+  return v;
+}
+
 template <typename T, int N, int SPT, int W, bool REAL = false>
 Variant tile_variant() {
   Variant v{};
