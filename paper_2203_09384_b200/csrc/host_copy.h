@@ -54,11 +54,19 @@ class CopyPool {
 
  private:
   CopyPool() {
-    // min(hardware threads, 16); SFFT_COPY_THREADS overrides.  Measured on
-    // the 16-core B200 host, 512 MiB each way: 8 threads 25.4 ms, 16 threads
-    // 23.0 ms, 24 threads 27.0 ms (host memory bandwidth is the wall).
+    // min(hardware threads / processes on this node, 16); SFFT_COPY_THREADS
+    // overrides.  Measured on the 16-core B200 host, 512 MiB each way:
+    // 8 threads 25.4 ms, 16 threads 23.0 ms, 24 threads 27.0 ms (host memory
+    // bandwidth is the wall).  Under torchrun every rank of the node runs its
+    // own pool, so the host's threads are split between them
+    // (LOCAL_WORLD_SIZE) instead of oversubscribed.
     const unsigned hw = std::thread::hardware_concurrency();
-    unsigned want = std::min(hw ? hw : 1u, 16u);
+    unsigned procs = 1;
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= 1024) procs = unsigned(v);
+    }
+    unsigned want = std::min(std::max((hw ? hw : 1u) / procs, 1u), 16u);
     if (const char* e = std::getenv("SFFT_COPY_THREADS")) {
       const int v = std::atoi(e);
       if (v >= 1 && v <= 64) want = unsigned(v);

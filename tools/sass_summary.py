@@ -107,6 +107,10 @@ def classify(demangled: str, sigs):
         label = (f"tile {m.group(1)} N={m.group(2)} spt={spt} warps={warps} "
                  f"{'inv' if m.group(5) == '1' else 'fwd'}{' real-in' if m.group(6) == '1' else ''}")
         return label, key in sigs
+    m = re.search(r"sfft::split2_kernel<(float|double), (\d+), (\d+), ([01]), (\d), (\d), ([01])>", d)
+    if m:
+        return (f"split2 {m.group(1)} N={m.group(2)} R={m.group(3)} {'inv' if m.group(4) == '1' else 'fwd'} "
+                f"layout={m.group(5)} twp={m.group(6)}{' real-in' if m.group(7) == '1' else ''}"), False
     m = re.search(r"sfft::stockham_pipe_kernel<(float|double), (\d+), (\d+), (\d+), ([01])", d)
     if m:
         return (f"stockham_pipe {m.group(1)} N={m.group(2)} R={m.group(3)} seq={m.group(4)} "
