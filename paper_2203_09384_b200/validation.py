@@ -48,8 +48,7 @@ def _screen(arr: np.ndarray, name: str, dtype) -> np.ndarray:
     if arr.dtype.kind not in _NUMERIC_KINDS:
         raise DomainError(f"{name} has non-numeric dtype {arr.dtype}")
     cast = arr.astype(dtype, copy=False)
-    finite = np.isfinite(cast.view(cast.real.dtype)) if np.iscomplexobj(cast) else np.isfinite(cast)
-    if not finite.all():
+    if not np.isfinite(cast).all():  # complex: finite iff both parts are
         raise DomainError(f"{name} contains NaN or Inf values")
     return cast
 
