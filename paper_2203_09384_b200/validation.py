@@ -116,14 +116,16 @@ def check_batch(length: int, shape, batch: int | None = None) -> int:
     tests/test_executor.py:95-100 expects).  ``batch`` is the plan's
     optional fixed row count.
     """
-    shape = tuple(int(s) for s in shape)
-    if len(shape) not in (1, 2):
-        raise ShapeError(f"signal must be (N,) or (batch, N), got shape {shape}")
+    ndim = len(shape)  # hot path of every execute(): plain indexing, no conversions
+    if ndim != 1 and ndim != 2:
+        raise ShapeError(f"signal must be (N,) or (batch, N), got shape {tuple(shape)}")
     if shape[-1] != length:
         raise ShapeError(f"signal length {shape[-1]} does not match plan length {length}")
-    rows = shape[0] if len(shape) == 2 else 1
+    if ndim == 1:
+        return 1
+    rows = int(shape[0])
     if rows == 0:
-        raise InvalidLengthError(f"signal batch is empty, shape {shape}")
-    if batch is not None and len(shape) == 2 and rows != batch:
+        raise InvalidLengthError(f"signal batch is empty, shape {tuple(shape)}")
+    if batch is not None and rows != batch:
         raise ShapeError(f"signal has {rows} rows; the plan was made for batch={batch}")
     return rows
