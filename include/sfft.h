@@ -154,7 +154,9 @@ int sfft_execute_sync_ex(sfft_plan_t plan, const void* d_in, void* d_out, int64_
 /* Synchronous execute on host memory: chunked H2D -> kernel -> D2H pipeline
  * over several streams (pinned memory gives full PCIe/C2C bandwidth);
  * calls up to 1 MiB take a single-stream latency path (pageable memory is
- * bounced through a pinned buffer).
+ * bounced through a pinned buffer).  The streams, device chunk buffers and
+ * pinned staging belong to the device, are shared by all plans on it and
+ * live as long as the process; host calls on one device run one at a time.
  * Returns SFFT_ERR_DOMAIN if the input held NaN/Inf (output then undefined). */
 int sfft_execute_host(sfft_plan_t plan, const void* h_in, void* h_out, int64_t batch);
 

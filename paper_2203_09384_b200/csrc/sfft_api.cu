@@ -210,21 +210,20 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-}  // namespace
-
-struct sfft_plan {
-  int32_t n = 0, precision = 0, direction = 0, device = 0, variant = 0;
-  int64_t batch = 0;
-  const Variant* v = nullptr;
-  void* d_tw = nullptr;
-  std::vector<unsigned char> host_base;  // base table in plan precision
-  // host-buffer pipeline state (lazily created, guarded by host_mu):
-  // one stream per engine (H2D copies, kernels, D2H copies) and `nslots`
-  // device chunk buffers cycled through them, ordered by per-slot events
-  std::mutex host_mu;
-  bool host_ready = false;
-  int64_t host_chunk_rows = 0;
+// Host-buffer pipeline of one device (sfft_execute_host*), shared by every
+// plan on that device and kept for the life of the process: one stream per
+// engine (H2D copies, kernels, D2H copies), `nslots` device chunk buffers
+// cycled through them and ordered by per-slot events, and the pinned
+// staging for pageable user memory.  Sharing it means a new plan's first
+// host call reuses the ~200 MB of pinned staging and device slots instead
+// of allocating its own (pinning costs ~1 ms per MiB on the B200 host:
+// tools/first_call_probe.py); calls on one device serialise on `mu`, which
+// costs nothing -- they would contend for the same host link anyway.
+struct HostPipeline {
+  std::mutex mu;
+  bool ready = false;
   int nslots = 0;
+  int64_t slot_bytes = 0;  // capacity of each device slot buffer
   cudaStream_t st_h2d = nullptr, st_kernel = nullptr, st_d2h = nullptr;
   cudaEvent_t ev_h2d[kMaxHostStreams] = {};  // slot's H2D done (kernel may read d_in)
   cudaEvent_t ev_k[kMaxHostStreams] = {};    // slot's kernel done (d_in free, D2H may read d_out)
@@ -234,11 +233,31 @@ struct sfft_plan {
   int32_t* h_flag = nullptr;  // pinned + mapped: kernels OR into it, host reads it
   int32_t* d_flag = nullptr;  // device alias of h_flag
   unsigned char* h_stage = nullptr;  // pinned bounce buffer for small pageable calls
-  int64_t h_stage_bytes = 0;
   // pinned per-slot chunk staging for large pageable calls
   unsigned char* h_chunk_in[kMaxHostStreams] = {};
   unsigned char* h_chunk_out[kMaxHostStreams] = {};
   int64_t h_chunk_bytes = 0;
+};
+
+// process-lifetime registry (never torn down: static destruction may run
+// after the CUDA runtime has unloaded)
+HostPipeline& host_pipeline(int device) {
+  static std::mutex registry_mu;
+  static std::vector<HostPipeline*> registry;
+  std::lock_guard<std::mutex> lock(registry_mu);
+  if (size_t(device) >= registry.size()) registry.resize(size_t(device) + 1, nullptr);
+  if (registry[size_t(device)] == nullptr) registry[size_t(device)] = new HostPipeline();
+  return *registry[size_t(device)];
+}
+
+}  // namespace
+
+struct sfft_plan {
+  int32_t n = 0, precision = 0, direction = 0, device = 0, variant = 0;
+  int64_t batch = 0;
+  const Variant* v = nullptr;
+  void* d_tw = nullptr;
+  std::vector<unsigned char> host_base;  // base table in plan precision
 };
 
 extern "C" {
@@ -360,22 +379,6 @@ int sfft_plan_destroy(sfft_plan_t p) {
   {
     DeviceGuard guard(p->device);
     if (p->d_tw) cudaFree(p->d_tw);
-    if (p->host_ready) {
-      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) {
-        cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
-      }
-      cudaFreeHost(p->h_flag);
-      for (int i = 0; i < kMaxHostStreams; ++i) {
-        cudaFree(p->d_in[i]);
-        cudaFree(p->d_out[i]);
-        if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
-        if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
-        for (cudaEvent_t ev : {p->ev_h2d[i], p->ev_k[i], p->ev_d2h[i]})
-          if (ev) cudaEventDestroy(ev);
-      }
-    }
-    if (p->h_stage) cudaFreeHost(p->h_stage);
   }
   delete p;
   return SFFT_OK;
@@ -545,26 +548,27 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   const LaunchFn launch = real ? p->v->launch_real[p->direction] : p->v->launch[p->direction];
   if (launch == nullptr)
     return fail(SFFT_ERR_ARGUMENT, "this plan's kernel has no real-input path (see sfft_plan_info.real_input)");
-  std::lock_guard<std::mutex> lock(p->host_mu);
+  HostPipeline& hp = host_pipeline(p->device);
+  std::lock_guard<std::mutex> lock(hp.mu);
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   // output rows are complex; real input rows carry half the bytes (H2D only)
   const int64_t row_bytes = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
   const int64_t in_row_bytes = real ? row_bytes / 2 : row_bytes;
   cudaError_t e = cudaSuccess;
-  if (!p->host_ready) {
-    p->nslots = host_shape().slots;
-    for (cudaStream_t* st : {&p->st_h2d, &p->st_kernel, &p->st_d2h})
+  if (!hp.ready) {
+    hp.nslots = host_shape().slots;
+    for (cudaStream_t* st : {&hp.st_h2d, &hp.st_kernel, &hp.st_d2h})
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
-    for (int i = 0; i < p->nslots && e == cudaSuccess; ++i)
-      for (cudaEvent_t* ev : {&p->ev_h2d[i], &p->ev_k[i], &p->ev_d2h[i]})
+    for (int i = 0; i < hp.nslots && e == cudaSuccess; ++i)
+      for (cudaEvent_t* ev : {&hp.ev_h2d[i], &hp.ev_k[i], &hp.ev_d2h[i]})
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e == cudaSuccess)
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_flag), sizeof(int32_t) * kMaxHostStreams,
+      e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_flag), sizeof(int32_t) * kMaxHostStreams,
                         cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_flag), p->h_flag, 0);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&hp.d_flag), hp.h_flag, 0);
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
-    p->host_ready = true;
+    hp.ready = true;
   }
   // chunks large enough for full-rate DMA, small enough to overlap copies in
   // both directions with the kernels of neighbouring chunks.
@@ -572,22 +576,23 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   const int64_t chunk_bytes = host_shape().chunk_bytes;
   const int64_t max_chunk_rows = chunk_bytes / row_bytes > 0 ? chunk_bytes / row_bytes : 1;
   const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
-  if (want_rows > p->host_chunk_rows) {
-    for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
-    for (int i = 0; i < p->nslots; ++i) {
-      cudaFree(p->d_in[i]);
-      cudaFree(p->d_out[i]);
-      p->d_in[i] = p->d_out[i] = nullptr;
+  const int64_t chunk_rows = want_rows;  // rows per pipeline chunk of this call
+  if (chunk_rows * row_bytes > hp.slot_bytes) {  // capacity in bytes: plans of any N share the slots
+    for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) cudaStreamSynchronize(st);
+    for (int i = 0; i < hp.nslots; ++i) {
+      cudaFree(hp.d_in[i]);
+      cudaFree(hp.d_out[i]);
+      hp.d_in[i] = hp.d_out[i] = nullptr;
     }
-    p->host_chunk_rows = 0;
-    for (int i = 0; i < p->nslots && e == cudaSuccess; ++i) {
-      e = cudaMalloc(&p->d_in[i], want_rows * row_bytes);
-      if (e == cudaSuccess) e = cudaMalloc(&p->d_out[i], want_rows * row_bytes);
+    hp.slot_bytes = 0;
+    for (int i = 0; i < hp.nslots && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&hp.d_in[i], chunk_rows * row_bytes);
+      if (e == cudaSuccess) e = cudaMalloc(&hp.d_out[i], chunk_rows * row_bytes);
     }
     if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
-    p->host_chunk_rows = want_rows;
+    hp.slot_bytes = chunk_rows * row_bytes;
   }
-  for (int i = 0; i < kMaxHostStreams; ++i) p->h_flag[i] = 0;
+  for (int i = 0; i < kMaxHostStreams; ++i) hp.h_flag[i] = 0;
   const int64_t total = batch * row_bytes;
   const int64_t total_in = batch * in_row_bytes;
 
@@ -595,22 +600,21 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     // latency path: one stream; pageable user memory goes through a pinned
     // bounce buffer (a host memcpy is cheaper than the driver's staging)
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
-    if (!pinned && p->h_stage == nullptr) {
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_stage), 2 * kSmallCallBytes, cudaHostAllocPortable);
+    if (!pinned && hp.h_stage == nullptr) {
+      e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_stage), 2 * kSmallCallBytes, cudaHostAllocPortable);
       if (e != cudaSuccess) return cuda_fail(e, "pinned staging allocation");
-      p->h_stage_bytes = 2 * kSmallCallBytes;
     }
     const void* src = h_in;
     void* dst = h_out;
     if (!pinned) {
-      std::memcpy(p->h_stage, h_in, size_t(total_in));
-      src = p->h_stage;
-      dst = p->h_stage + kSmallCallBytes;
+      std::memcpy(hp.h_stage, h_in, size_t(total_in));
+      src = hp.h_stage;
+      dst = hp.h_stage + kSmallCallBytes;
     }
-    cudaStream_t st = p->st_h2d;
-    e = cudaMemcpyAsync(p->d_in[0], src, size_t(total_in), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = launch(p->d_in[0], p->d_out[0], p->d_tw, batch, p->d_flag, st, false);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, p->d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
+    cudaStream_t st = hp.st_h2d;
+    e = cudaMemcpyAsync(hp.d_in[0], src, size_t(total_in), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch(hp.d_in[0], hp.d_out[0], p->d_tw, batch, hp.d_flag, st, false);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, hp.d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
     if (!pinned) std::memcpy(h_out, dst, size_t(total));
@@ -628,46 +632,46 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     const unsigned char* src = static_cast<const unsigned char*>(h_in);
     unsigned char* dst = static_cast<unsigned char*>(h_out);
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
-    const int S = p->nslots;
-    const int64_t stage_bytes = p->host_chunk_rows * row_bytes;
-    if (!pinned && p->h_chunk_bytes < stage_bytes) {
-      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
+    const int S = hp.nslots;
+    const int64_t stage_bytes = chunk_rows * row_bytes;
+    if (!pinned && hp.h_chunk_bytes < stage_bytes) {
+      for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) cudaStreamSynchronize(st);
       for (int i = 0; i < S; ++i) {
-        if (p->h_chunk_in[i]) cudaFreeHost(p->h_chunk_in[i]);
-        if (p->h_chunk_out[i]) cudaFreeHost(p->h_chunk_out[i]);
-        p->h_chunk_in[i] = p->h_chunk_out[i] = nullptr;
+        if (hp.h_chunk_in[i]) cudaFreeHost(hp.h_chunk_in[i]);
+        if (hp.h_chunk_out[i]) cudaFreeHost(hp.h_chunk_out[i]);
+        hp.h_chunk_in[i] = hp.h_chunk_out[i] = nullptr;
       }
-      p->h_chunk_bytes = 0;
+      hp.h_chunk_bytes = 0;
       for (int i = 0; i < S && e == cudaSuccess; ++i) {
-        e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_in[i]), stage_bytes, cudaHostAllocPortable);
+        e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_chunk_in[i]), stage_bytes, cudaHostAllocPortable);
         if (e == cudaSuccess)
-          e = cudaHostAlloc(reinterpret_cast<void**>(&p->h_chunk_out[i]), stage_bytes, cudaHostAllocPortable);
+          e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_chunk_out[i]), stage_bytes, cudaHostAllocPortable);
       }
       if (e != cudaSuccess) return cuda_fail(e, "pinned chunk staging allocation");
-      p->h_chunk_bytes = stage_bytes;
+      hp.h_chunk_bytes = stage_bytes;
     }
     auto& pool = sfft_host::CopyPool::instance();
     // a failure mid-pipeline drains the streams before returning, so the next
     // call never races leftover copies on the slot buffers
     auto fail_sync = [&](cudaError_t err, const char* what) {
-      for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) cudaStreamSynchronize(st);
+      for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) cudaStreamSynchronize(st);
       return cuda_fail(err, what);
     };
     // staged (pageable) path: which rows each slot's host staging holds
     int64_t slot_row[kMaxHostStreams] = {}, slot_rows[kMaxHostStreams] = {};
     auto drain_slot = [&](int s) -> cudaError_t {
       if (slot_rows[s] == 0) return cudaSuccess;
-      const cudaError_t err = cudaEventSynchronize(p->ev_d2h[s]);
+      const cudaError_t err = cudaEventSynchronize(hp.ev_d2h[s]);
       if (err != cudaSuccess) return err;
-      pool.memcpy(dst + slot_row[s] * row_bytes, p->h_chunk_out[s], size_t(slot_rows[s] * row_bytes));
+      pool.memcpy(dst + slot_row[s] * row_bytes, hp.h_chunk_out[s], size_t(slot_rows[s] * row_bytes));
       slot_rows[s] = 0;
       return cudaSuccess;
     };
     int chunk = 0;
-    for (int64_t row = 0; row < batch; row += p->host_chunk_rows, ++chunk) {
+    for (int64_t row = 0; row < batch; row += chunk_rows, ++chunk) {
       const int s = chunk % S;
       const bool reuse = chunk >= S;  // the slot's previous chunk is in flight
-      const int64_t rows = batch - row < p->host_chunk_rows ? batch - row : p->host_chunk_rows;
+      const int64_t rows = batch - row < chunk_rows ? batch - row : chunk_rows;
       const size_t bytes = size_t(rows * row_bytes);
       const size_t in_bytes = size_t(rows * in_row_bytes);
       const void* h2d_src = src + row * in_row_bytes;
@@ -677,23 +681,23 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
         // done implies its H2D done)
         e = drain_slot(s);
         if (e != cudaSuccess) return fail_sync(e, "staging drain");
-        pool.memcpy(p->h_chunk_in[s], src + row * in_row_bytes, in_bytes);
-        h2d_src = p->h_chunk_in[s];
-        d2h_dst = p->h_chunk_out[s];
+        pool.memcpy(hp.h_chunk_in[s], src + row * in_row_bytes, in_bytes);
+        h2d_src = hp.h_chunk_in[s];
+        d2h_dst = hp.h_chunk_out[s];
       }
-      if (reuse) e = cudaStreamWaitEvent(p->st_h2d, p->ev_k[s], 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_in[s], h2d_src, in_bytes, cudaMemcpyHostToDevice, p->st_h2d);
-      if (e == cudaSuccess) e = cudaEventRecord(p->ev_h2d[s], p->st_h2d);
+      if (reuse) e = cudaStreamWaitEvent(hp.st_h2d, hp.ev_k[s], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hp.d_in[s], h2d_src, in_bytes, cudaMemcpyHostToDevice, hp.st_h2d);
+      if (e == cudaSuccess) e = cudaEventRecord(hp.ev_h2d[s], hp.st_h2d);
       if (e != cudaSuccess) return fail_sync(e, "H2D copy");
-      e = cudaStreamWaitEvent(p->st_kernel, p->ev_h2d[s], 0);
-      if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(p->st_kernel, p->ev_d2h[s], 0);
+      e = cudaStreamWaitEvent(hp.st_kernel, hp.ev_h2d[s], 0);
+      if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(hp.st_kernel, hp.ev_d2h[s], 0);
       if (e == cudaSuccess)
-        e = launch(p->d_in[s], p->d_out[s], p->d_tw, rows, p->d_flag + s, p->st_kernel, false);
-      if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[s], p->st_kernel);
+        e = launch(hp.d_in[s], hp.d_out[s], p->d_tw, rows, hp.d_flag + s, hp.st_kernel, false);
+      if (e == cudaSuccess) e = cudaEventRecord(hp.ev_k[s], hp.st_kernel);
       if (e != cudaSuccess) return fail_sync(e, "kernel launch");
-      e = cudaStreamWaitEvent(p->st_d2h, p->ev_k[s], 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(d2h_dst, p->d_out[s], bytes, cudaMemcpyDeviceToHost, p->st_d2h);
-      if (e == cudaSuccess) e = cudaEventRecord(p->ev_d2h[s], p->st_d2h);
+      e = cudaStreamWaitEvent(hp.st_d2h, hp.ev_k[s], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(d2h_dst, hp.d_out[s], bytes, cudaMemcpyDeviceToHost, hp.st_d2h);
+      if (e == cudaSuccess) e = cudaEventRecord(hp.ev_d2h[s], hp.st_d2h);
       if (e != cudaSuccess) return fail_sync(e, "D2H copy");
       if (!pinned) {
         slot_row[s] = row;
@@ -707,13 +711,13 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
         if (e != cudaSuccess) return fail_sync(e, "staging drain");
       }
     }
-    for (cudaStream_t st : {p->st_h2d, p->st_kernel, p->st_d2h}) {
+    for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) {
       e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return cuda_fail(e, "stream sync");
     }
   }
   for (int i = 0; i < kMaxHostStreams; ++i)
-    if (reinterpret_cast<volatile int32_t*>(p->h_flag)[i])
+    if (reinterpret_cast<volatile int32_t*>(hp.h_flag)[i])
       return fail(SFFT_ERR_DOMAIN, "signal contains NaN or Inf values");
   return SFFT_OK;
 }
