@@ -322,3 +322,22 @@ def test_more_than_2_31_elements(cuda, prec, n):
     del x, y
     torch.cuda.empty_cache()
     assert row_rel_l2(got, oracle.direct_dft(xs)).max() <= tolerance(n, prec)
+
+
+def test_host_pipeline_shared_across_plans(cuda):
+    """sfft_execute_host keeps one pipeline per device (streams, slots, pinned
+    staging) shared by every plan: interleaved plans of different row sizes,
+    chunked and small calls, pageable and pinned buffers, all bit-identical
+    to the device path."""
+    specs = [(8, "single", "forward", (40 << 20) // 64 + 7), (2048, "double", "inverse", (40 << 20) // (2048 * 16) + 3),
+             (64, "single", "inverse", 100), (1024, "double", "forward", (70 << 20) // (1024 * 16) + 1),
+             (2, "double", "forward", 5)]
+    cases = []
+    for n, prec, direction, rows in specs:
+        x = sf.generate_batch(rows, n, seed=n, precision=prec)
+        plan = sf.make_plan(n, direction, precision=prec)
+        cases.append((plan, x, run(plan, x, cuda)))
+    for rep in range(2):
+        for plan, x, want in cases:
+            got = sf.execute(plan, x if rep == 0 else torch.from_numpy(x).pin_memory().numpy())
+            assert np.array_equal(got, want)
