@@ -1,6 +1,6 @@
 // Batched C2C FFT kernels for sm_100a.
 //
-// Two kernel families cover N = 2 .. 2048 in fp32 and fp64:
+// Kernel families covering N = 2 .. 2048 in fp32 and fp64:
 //
 // * stockham_kernel  (N >= 64 fp32, N >= 32 fp64)
 //   G = N/R threads own one sequence; each thread keeps R elements in
@@ -10,7 +10,12 @@
 //   between passes goes through padded or row-swizzled (bank-conflict-free)
 //   shared memory, and the last pass writes straight to HBM in natural order
 //   (Stockham autosort: no digit-reversal gather, cf. executor.py:77).
-//   One HBM read + one HBM write per element.
+//   One HBM read + one HBM write per element.  With R = 32 / 64 a sequence
+//   is one warp (two passes, __syncwarp only) -- the round-2 defaults for
+//   fp32 N = 2048 and fp64 N = 512, 1024.
+//
+// * split2_kernel    (tested variant, fp64 N = 2048): two one-warp N/2
+//   transforms of the polyphase halves plus a radix-2 combine.
 //
 // * tile_kernel      (N <= 32 fp32, N <= 16 fp64)
 //   One thread owns whole sequences.  A warp stages a contiguous tile of
@@ -20,7 +25,7 @@
 //   with 16-byte coalesced stores.  fp32 N = 2 (one 16-byte chunk per
 //   sequence) skips the staging altogether.
 //
-// Both fuse: the inverse direction (swap trick), the 1/N inverse scale
+// All fuse: the inverse direction (swap trick), the 1/N inverse scale
 // (executor.py:93-94; exact for powers of two) and the non-finite input
 // check (executor.py:72-73) into the single pass over HBM.
 #pragma once
@@ -438,7 +443,7 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
 // Twiddles: the N/2 transform's per-pass table, then w_N^k for k < N/2 --
 // exactly the generic per-pass table of the pass list [R, ..., 2].
 template <typename T, int N, int R, bool INV, int LAYOUT, int TWP, bool RIN = false>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(64, 6)  // <= 168 registers: 6 CTAs (12 warps) per SM
 split2_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
               const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
   using C = cx_t<T>;

@@ -23,10 +23,11 @@ std::vector<Variant> table_f64_2048(int log2n) {
           // box-to-box noise, so entry 0 stays (profiles/r02_wide_radix_study.txt)
           stockham_variant<double, 2048, 32, 1, 2, 1, 1, true>(),
           stockham_variant<double, 2048, 32, 1, 2, 1, 0>(),  // R32, LDG
-          // two one-warp N/2 transforms + radix-2 combine (split2_kernel): real
-          // input 6.26 vs 5.66 TB/s, but complex 6.27 vs 6.94 burst and 0.84 vs
-          // 0.90 of the sustained copy (2 warps per 32 KB CTA: half the warps
-          // per SM) -- kept as a tested variant (profiles/r02_wide_radix_study.txt)
+          // two one-warp N/2 transforms + radix-2 combine (split2_kernel, 6 CTAs
+          // per SM): burst 6811 vs 6944 GB/s (-1.9 %), sustained 0.905 vs 0.897 of
+          // the copy, real input 6.28 vs 5.67 TB/s -- a wash on the complex path,
+          // so entry 0 stays; the real path must use the complex path's kernel to
+          // stay bit-identical to widening (profiles/r02_wide_radix_study.txt)
           split2_variant<double, 2048, 32, 2, 1, true>(),
       };
     default:
