@@ -9,14 +9,7 @@ std::vector<Variant> table_f64_2048(int log2n) {
   switch (log2n) {
     case 11:
       return {
-          // default (round 2): two one-warp N/2 transforms + radix-2 combine
-          // (split2_kernel, 6 CTAs = 12 warps per SM).  Against the R16 kernel
-          // (entry 1): sustained power-capped load +1 to +2 % (0.92 vs 0.91 of
-          // the copy's own rate; interleaved A/B +3 %), real input 6.28 vs 5.67
-          // TB/s, error 5.42e-16 vs 5.51e-16; burst -1.9 % (6811 vs 6944 GB/s,
-          // still 1.04x copy) (profiles/r02_wide_radix_study.txt).
-          split2_variant<double, 2048, 32, 2, 1, true>(),
-          stockham_variant<double, 2048, 16, 1, 2, 1, 1>(),  // round-1 default (R16, [16,16,8], bulk TMA)
+          stockham_variant<double, 2048, 16, 1, 2, 1, 1, true>(),
           stockham_variant<double, 2048, 16, 1, 2>(),
           stockham_variant<double, 2048, 8, 1, 2, 1>(),
           stockham_variant<double, 2048, 16, 1, 1>(),
@@ -25,8 +18,19 @@ std::vector<Variant> table_f64_2048(int log2n) {
           stockham_variant<double, 2048, 16, 1, 2, 2, 1>(),  // TWP 2 + bulk TMA
           stockham_variant<double, 2048, 16, 1, 2, 0, 1>(),  // TWP 0 + bulk TMA
           pipe_variant<double, 2048, 16, 1, 2, 1, 2>(),      // 2-stage pipeline (64 KB, 3 CTAs/SM)
-          stockham_variant<double, 2048, 32, 1, 2, 1, 1>(),  // R32 (passes [32, 32, 2], two warps) + bulk TMA
+          // R32 (passes [32, 32, 2], two warps per sequence) + bulk TMA: +1.2 %
+          // sustained, -1.2 % burst, +5 % real input against entry 0 -- within
+          // box-to-box noise, so entry 0 stays (profiles/r02_wide_radix_study.txt)
+          stockham_variant<double, 2048, 32, 1, 2, 1, 1, true>(),
           stockham_variant<double, 2048, 32, 1, 2, 1, 0>(),  // R32, LDG
+          // two one-warp N/2 transforms + radix-2 combine (split2_kernel, 6 CTAs
+          // per SM).  Against entry 0: sustained +1 to +3 %, real input 6.28 vs
+          // 5.67 TB/s, burst -1.9 %, and its polyphase gather reads every other
+          // 16-byte element of the linear TMA staging (2-way bank conflict: 25 %
+          // excess shared wavefronts); staging with a per-row skew removes the
+          // conflict but needs 256 small bulk copies per row, which cut the rate
+          // to 5.76 TB/s.  Kept as a tested variant (profiles/r02_wide_radix_study.txt).
+          split2_variant<double, 2048, 32, 2, 1, true>(),
       };
     default:
       return {};

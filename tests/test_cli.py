@@ -49,7 +49,7 @@ def test_npy_batch_round_trip_and_errors(tmp_path):
 def test_plan_command(capsys):
     assert main(["plan", "--length", "2048", "--precision", "double"]) == 0
     out = capsys.readouterr().out
-    assert "stages: 8,8,8,4" in out and "precision: double" in out and "gpu_kernel: split2" in out and "gpu_passes: 32,32,2" in out
+    assert "stages: 8,8,8,4" in out and "precision: double" in out and "gpu_passes: 16,16,8" in out
 
 
 def test_exit_codes(capsys):

@@ -15,11 +15,11 @@ timeout 600 python tests/accuracy_report.py gpurun_out/accuracy.json > gpurun_ou
 NS=2,8,32,64,256,512,1024,2048 timeout 600 python tools/real_input_probe.py > gpurun_out/real_input.jsonl 2>&1
 B="python bench.py --steps 4 --warmup 3 --no-cpu --no-extras --e2e-steps 1 --no-check"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 10 --warmup 3 --no-cpu --no-extras --e2e-steps 1 --no-check > gpurun_out/ncu_launch_run.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_c2 $B > gpurun_out/ncu_c2.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_c4 $B --config c4 > gpurun_out/ncu_c4.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_c5 $B --config c5 > gpurun_out/ncu_c5.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_f2048 $B --n 2048 --precision single > gpurun_out/ncu_f2048.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stockham -s 3 -c 1 -o gpurun_out/prof_d1024 $B --n 1024 --precision double > gpurun_out/ncu_d1024.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stockham|split2" -s 3 -c 1 -o gpurun_out/prof_c2 $B > gpurun_out/ncu_c2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stockham|split2" -s 3 -c 1 -o gpurun_out/prof_c4 $B --config c4 > gpurun_out/ncu_c4.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stockham|split2" -s 3 -c 1 -o gpurun_out/prof_c5 $B --config c5 > gpurun_out/ncu_c5.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stockham|split2" -s 3 -c 1 -o gpurun_out/prof_f2048 $B --n 2048 --precision single > gpurun_out/ncu_f2048.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stockham|split2" -s 3 -c 1 -o gpurun_out/prof_d1024 $B --n 1024 --precision double > gpurun_out/ncu_d1024.log 2>&1
 timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/sanitizer_memcheck.txt 2>&1
 timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_run.py --quick > gpurun_out/sanitizer_racecheck.txt 2>&1
 timeout 600 compute-sanitizer --tool synccheck python tools/sanitize_run.py --quick > gpurun_out/sanitizer_synccheck.txt 2>&1
