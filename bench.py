@@ -523,9 +523,12 @@ def run_gpu(args, n, batch, precision, direction, workload):
     for _ in range(min(args.warmup, 2)):
         sf.execute(plan, hin_np, out=hout_np)
     barrier()
+    step_s = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
+        ts = time.perf_counter()
         sf.execute(plan, hin_np, out=hout_np)
+        step_s.append(time.perf_counter() - ts)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     if rank == 0 and not args.no_check:
         assert np.array_equal(hout_np[:64], y[:64].cpu().numpy()), "e2e output differs from device output"
@@ -582,6 +585,9 @@ def run_gpu(args, n, batch, precision, direction, workload):
             "link": link,
             "link_bound_ms_per_step": round(link_bound_s * 1e3, 3),
             "frac_of_link_bound": round(link_bound_s / e2e_s, 4),
+            # this rank's individual steps (value above = their mean, max over ranks)
+            "step_ms_min_median_max": [round(min(step_s) * 1e3, 3), round(statistics.median(step_s) * 1e3, 3),
+                                       round(max(step_s) * 1e3, 3)],
         },
         "roofline": {
             "bound": "hbm",
