@@ -610,9 +610,14 @@ def run_gpu(args, n, batch, precision, direction, workload):
         "parity_rel_l2_max_first64_vs_numpy_c128": parity,
     }
     if world == 1 and not args.no_extras:
-        # BASELINE configs[2] and [3] under the same clock record as `value`
-        out["sweep"] = run_sweep(sf, dev, stream, clocks, peak)
-        out["c4"] = run_c4(sf, dev, stream, clocks, peak)
+        # BASELINE configs[2] and [3] under the same clock record as `value`;
+        # a failure here (e.g. a smaller device) must not cost the main line
+        for key, fn in (("sweep", run_sweep), ("c4", run_c4)):
+            try:
+                out[key] = fn(sf, dev, stream, clocks, peak)
+            except Exception as exc:  # noqa: BLE001 - reported in the line instead
+                out[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                torch.cuda.empty_cache()
     clocks.stop()
     barrier()  # every rank's GPU work is done before rank 0 loads the host
     if rank == 0 and not args.no_cpu:
