@@ -1,9 +1,12 @@
 """Run the reference's own test suite (pkg/tests, 285 tests) against this package.
 
 ``stagefft`` and its submodules are aliased to ``paper_2203_09384_b200`` so
-the reference's tests import this package unchanged; every test here is
-marked ``gpu`` because ``execute`` has no CPU fallback.  The suite itself is
-materialised by ``materialize.py`` (git-ignored copy of the reference files).
+the reference's tests import this package unchanged.  The tests listed in
+``needs_gpu.txt`` (they call ``execute`` and friends, which have no CPU
+fallback) are marked ``gpu``; the rest -- planner, numerics, signal files,
+statistics, record/summary logic, ... -- run in the CPU suite as well.  The
+suite itself is materialised by ``materialize.py`` (git-ignored copy of the
+reference files).
 
 ``DEVIATIONS`` lists every reference test this package fails on purpose, with
 the reason; each is marked ``xfail(strict=True)``, so a deviation that stops
@@ -46,13 +49,23 @@ DEVIATIONS: dict[str, str] = {
 }
 
 
+def _needs_gpu() -> frozenset:
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "needs_gpu.txt")
+    with open(path) as f:
+        return frozenset(line.strip() for line in f if line.strip() and not line.startswith("#"))
+
+
+NEEDS_GPU = _needs_gpu()
+
+
 def pytest_collection_modifyitems(config, items):
     here = os.path.dirname(os.path.abspath(__file__))
     for item in items:
         if not str(item.fspath).startswith(here):
             continue
-        item.add_marker(pytest.mark.gpu)
         key = f"{os.path.basename(str(item.fspath))}::{item.name}"
+        if key in NEEDS_GPU:
+            item.add_marker(pytest.mark.gpu)
         reason = DEVIATIONS.get(key)
         if reason is not None:
             item.add_marker(pytest.mark.xfail(reason=reason, strict=True))
