@@ -33,6 +33,10 @@ from .numerics import TwiddleTable, is_power_of_two
 from .planner import Algorithm, Direction, FftPlan, digit_reversal_permutation, make_plan
 
 
+#: 1/sqrt(2), the radix-8 stage constant (kernels.py:25, :136-141); the GPU
+#: kernels use the same value as a compile-time constant (sfft_device.cuh).
+SQRT1_2 = float(np.sqrt(0.5))
+
 # ------------------------------------------------------------ stage level
 @dataclass
 class StageBuffer:
