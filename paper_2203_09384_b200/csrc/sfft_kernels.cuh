@@ -330,6 +330,36 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
   });
 }
 
+// Output-side NaN/Inf check (the out-of-place default of the Stockham and
+// split2 kernels).  X[0] = sum of all N inputs, formed by additions alone
+// (every k = 0 twiddle is exactly 1), so a non-finite input always makes
+// X[0] non-finite (Inf - Inf = NaN, NaN + x = NaN): one test of X[0] by the
+// thread that owns it replaces a test of every input (for fp64 that input
+// test costs ~3 instructions per element: packing the high words for FFMA2).
+// X[0] can also overflow from finite inputs, so a hit re-reads the row's
+// inputs and reports only a truly non-finite one -- the reference's
+// input-side semantics (executor.py:72-73).  In-place launches overwrite the
+// inputs, so they keep the input-side check at load time.
+template <typename C>
+__device__ __forceinline__ bool cx_finite(C v) {
+  return isfinite(v.x) && isfinite(v.y);
+}
+template <typename In>
+__device__ __noinline__ void recheck_row_inputs(const In* __restrict__ row, int n, int* nonfinite) {
+  for (int i = 0; i < n; ++i) {
+    bool ok;
+    if constexpr (std::is_same_v<In, float> || std::is_same_v<In, double>) {
+      ok = isfinite(row[i]);
+    } else {
+      ok = cx_finite(row[i]);
+    }
+    if (!ok) {
+      atomicOr(nonfinite, 1);
+      return;
+    }
+  }
+}
+
 template <typename T, int R>
 __device__ __forceinline__ void check_nonfinite(const cx_t<T> (&v)[R], int* nonfinite) {
   float2 acc = make_float2(0.f, 0.f);
@@ -417,11 +447,16 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
       for (int m = 0; m < R; ++m) v[m] = ld_stream(src + m * G);
     }
   }
-  if (nonfinite != nullptr && valid) check_nonfinite<T, R>(v, nonfinite);
+  // NaN/Inf check: on X[0] after the passes (out-of-place), on the loaded
+  // inputs when the launch is in place (see recheck_row_inputs)
+  const bool in_place = static_cast<const void*>(in) == static_cast<const void*>(out);
+  if (nonfinite != nullptr && valid && in_place) check_nonfinite<T, R>(v, nonfinite);
   // LAYOUT 1 keeps each sequence in its own padded region; LAYOUT 2 swizzles
   // the CTA-wide element index (sequences are N apart, N a multiple of R).
   stockham_passes<T, N, R, SEQ, INV, LAYOUT, TWP>(v, LAYOUT == 1 ? sm + s * SN : sm, LAYOUT == 1 ? 0 : s * N, j,
                                                   s, valid ? out + seq * N : nullptr, tw);
+  if (nonfinite != nullptr && valid && !in_place && j == 0 && !cx_finite(v[0]))
+    recheck_row_inputs(in + seq * N, N, nonfinite);
 }
 
 // Two-warp kernel for N = 2 * 32 * R (fp64 N = 2048 with R = 32): one level of
@@ -485,7 +520,8 @@ split2_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T
     for (int m = 0; m < R; ++m) v[m] = sm[2 * (j + m * G) + w];
   }
   __syncthreads();  // staging fully read before the exchange regions reuse it
-  if (nonfinite != nullptr) check_nonfinite<T, R>(v, nonfinite);
+  const bool in_place = static_cast<const void*>(in) == static_cast<const void*>(out);
+  if (nonfinite != nullptr && in_place) check_nonfinite<T, R>(v, nonfinite);
   if constexpr (INV) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
@@ -520,6 +556,9 @@ split2_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T
     st_stream(dst + k + H, y1);
   };
   if (w == 0) {
+    // X[0] = E[0] + O[0]: the out-of-place NaN/Inf check (see recheck_row_inputs)
+    if (nonfinite != nullptr && !in_place && j == 0 && !cx_finite(cadd(v[0], xs[j])))
+      recheck_row_inputs(in + seq * N, N, nonfinite);
 #pragma unroll
     for (int m = 0; m < HR; ++m) combine(v[m], xs[m * 32 + j], j + m * G);
   } else {
@@ -564,6 +603,7 @@ stockham_pipe_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
   const int j = tid - s * G;
   const long long ntiles = (batch + SEQ - 1) / SEQ;
   const long long step = gridDim.x;
+  const bool in_place = static_cast<const void*>(in) == static_cast<const void*>(out);
   pdl_enter();
 
   auto issue = [&](long long tile, int b) {  // one thread
@@ -600,10 +640,12 @@ stockham_pipe_kernel(const cx_t<T>* __restrict__ in, cx_t<T>* __restrict__ out,
     C v[R];
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = buf[s * N + j + m * G];  // linear staging, conflict-free
-    if (nonfinite != nullptr && valid) check_nonfinite<T, R>(v, nonfinite);
+    if (nonfinite != nullptr && valid && in_place) check_nonfinite<T, R>(v, nonfinite);
     __syncthreads();  // staging fully read before the exchange layout reuses it
     stockham_passes<T, N, R, SEQ, INV, LAYOUT, TWP>(v, LAYOUT == 1 ? buf + s * SN : buf, LAYOUT == 1 ? 0 : s * N,
                                                     j, s, valid ? out + seq * N : nullptr, tw);
+    if (nonfinite != nullptr && valid && !in_place && j == 0 && !cx_finite(v[0]))
+      recheck_row_inputs(in + seq * N, N, nonfinite);
     // every generic-proxy access to `buf` is done before the async proxy
     // (the refill issued at the top of the next iteration) overwrites it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

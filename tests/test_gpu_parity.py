@@ -341,3 +341,42 @@ def test_host_pipeline_shared_across_plans(cuda):
         for plan, x, want in cases:
             got = sf.execute(plan, x if rep == 0 else torch.from_numpy(x).pin_memory().numpy())
             assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_nonfinite_detection_every_variant(cuda, prec):
+    """The Stockham/split2 kernels test X[0] (the sum of every input) after the
+    passes instead of every input; in-place launches test the inputs.  Every
+    variant, both directions, NaN/Inf in the first, a middle and the last row
+    of an odd batch (partial CTA), real input where supported -- and finite
+    rows whose X[0] overflows must NOT raise (the reference checks inputs)."""
+    lib = sf._native.lib()
+    code = 0 if prec == "single" else 1
+    dt = dtype_of(prec)
+    big = 3.0e37 if prec == "single" else 1.0e306  # finite, but N of them overflow
+    for n in ALL_N:
+        for v in range(lib.sfft_num_variants(n, code)):
+            info = sf._native.variant_info(n, code, v)
+            for direction in DIRS:
+                plan = sf.make_plan(n, direction, precision=prec, variant=v)
+                for row, col, val in ((0, 0, np.inf), (150, n // 2, complex(0, np.nan)), (300, n - 1, -np.inf)):
+                    x = np.ones((301, n), dt)
+                    x[row, col] = val
+                    xd = torch.from_numpy(x).to(cuda)
+                    with pytest.raises(sf.DomainError):
+                        sf.execute(plan, xd)
+                    flag = torch.zeros(1, dtype=torch.int32, device=cuda)
+                    buf = xd.clone()
+                    sf.launch(plan, buf, buf, 301, flag=flag)  # in place
+                    torch.cuda.synchronize()
+                    assert int(flag.item()) == 1, (n, v, direction, row)
+                    if info["real_input"] and row == 0:
+                        xr = torch.ones((301, n), dtype=torch.float32 if prec == "single" else torch.float64,
+                                        device=cuda)
+                        xr[300, 0] = float("nan")
+                        with pytest.raises(sf.DomainError):
+                            sf.execute(plan, xr)
+                if n >= 1024:
+                    x = np.full((7, n), big, dt)
+                    y = sf.execute(plan, torch.from_numpy(x).to(cuda)).cpu().numpy()
+                    assert not np.isfinite(y[:, 0]).all()  # X[0] overflowed, no DomainError
