@@ -71,7 +71,7 @@ typedef struct sfft_plan_info {
   int32_t radices[8];          /* GPU pass radices, first to last */
   int64_t twiddle_elems;       /* per-pass twiddle table length (elements) */
   int32_t variant;             /* index into the kernel variant table */
-  int32_t layout;              /* stockham smem layout: 1 padded, 2 row swizzle */
+  int32_t layout;              /* stockham smem layout: 1 padded, 2 row swizzle, 3 split re/im exchange (fp64) */
   int32_t twiddle_policy;      /* 0: every twiddle loaded; 1: powers of two + products */
   int32_t loader;              /* 0: per-thread global loads; 1: one bulk TMA copy per CTA;
                                   2: persistent CTAs, pipelined bulk TMA copies */

@@ -85,14 +85,24 @@ __host__ __device__ constexpr int twiddle_table_len(int n, int r) {
 //           swizzle of e with higher bits of e) and
 //           no padding (16-byte accesses stay 128-byte aligned per phase,
 //           which LAYOUT 1 breaks).
+// LAYOUT 3: fp64 only -- the exchange moves the real parts, then the
+//           imaginary parts, through an N-double region (half the bytes of
+//           LAYOUT 2) indexed like LAYOUT 2 with 8-byte words (W = 16).  Same
+//           wavefronts per exchange, two more barriers, and half the shared
+//           memory per sequence: with per-thread loads (LOADER 0) the shared
+//           memory holds only the exchange, so the L1 keeps room for the
+//           loads in flight and no bulk copy writes + gathers the row through
+//           the shared-memory pipe.
 // tests/test_bank_model.py replays every access of every variant per phase.
 template <typename T, int LAYOUT, int R>
 struct Smem {
-  static constexpr int W = sizeof(T) == 4 ? 16 : 8;  // complex elements per 128-byte row
+  static constexpr int W = (sizeof(T) == 4 || LAYOUT == 3) ? 16 : 8;  // words (complex or LAYOUT-3 halves) per 128-byte row
   static constexpr int LGR = ilog2(R);
-  static_assert(LAYOUT == 1 || LAYOUT == 2, "smem layout");
-  static_assert(LAYOUT != 2 || R >= W, "row swizzle needs R >= elements per bank row");
-  __host__ __device__ static constexpr int size(int n) { return LAYOUT == 1 ? n + n / R : n; }
+  static_assert(LAYOUT == 1 || LAYOUT == 2 || LAYOUT == 3, "smem layout");
+  static_assert(LAYOUT == 1 || R >= W, "row swizzle needs R >= elements per bank row");
+  static_assert(LAYOUT != 3 || sizeof(T) == 8, "split exchange: fp64 only");
+  // in complex elements (LAYOUT 3 stores N doubles = N/2 complex)
+  __host__ __device__ static constexpr int size(int n) { return LAYOUT == 1 ? n + n / R : (LAYOUT == 3 ? n / 2 : n); }
   __device__ static __forceinline__ int map(int e) {
     if constexpr (LAYOUT == 1) {
       return e + e / R;
@@ -107,8 +117,8 @@ struct Smem {
     if constexpr (LAYOUT == 1) {
       if (off % R == 0) return mapped_base + off + off / R;
       if (base_aligned && off < R) return mapped_base + off;
-    } else if constexpr (LAYOUT == 2) {
-      // identical subexpressions per residue are CSE'd across the unrolled pass
+    } else {
+      // LAYOUT 2 / 3; identical subexpressions per residue are CSE'd across the unrolled pass
       if (off % R == 0) return (base ^ (((base >> LGR) + ((off >> LGR) & (W - 1))) & (W - 1))) + off;
       if (base_aligned && off < R) return base + ((off & (W - 1)) ^ ((base >> LGR) & (W - 1))) + (off & ~(W - 1));
     }
@@ -205,6 +215,22 @@ __device__ __forceinline__ void apply_pass_twiddles(C (&v)[R], const C* __restri
       }
       v[t + q * NB] = cmul(v[t + q * NB], w[q]);
     });
+  } else if constexpr (TWP == 3) {
+    // one load per butterfly: w^(2^i) by repeated squaring, the rest as in
+    // TWP 1 (<= ~8 ulp; trades L1 data-pipe wavefronts for FP64 products)
+    C w[r];
+    static_for<1, r>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      if constexpr (q == 1) {
+        w[q] = __ldg(tp);
+      } else if constexpr ((q & (q - 1)) == 0) {
+        w[q] = cmul(w[q / 2], w[q / 2]);
+      } else {
+        constexpr int hi = high_pow2(q);
+        w[q] = cmul(w[hi], w[q - hi]);
+      }
+      v[t + q * NB] = cmul(v[t + q * NB], w[q]);
+    });
   } else {
     C w[r];
     static_for<1, r>([&](auto Q) {
@@ -271,6 +297,8 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
   }
+  constexpr bool SPLIT = (LAYOUT == 3);  // exchange real parts, then imaginary parts
+  T* __restrict__ sq = reinterpret_cast<T*>(smq);
   const int rbase = sbase + j;
   const int rbase_m = S::map(rbase);
 
@@ -280,9 +308,12 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
     constexpr int L = pass_stride(N, R, p);
     constexpr int NB = R / r;  // butterflies per thread in this pass
     if constexpr (p > 0) {
-      // gather this pass's inputs x[j + m*G] from the exchange buffer
+      // gather this pass's inputs x[j + m*G] from the exchange buffer (the
+      // split exchange gathered them at the end of the previous pass)
+      if constexpr (!SPLIT) {
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = smq[S::map2(rbase, rbase_m, m * G)];
+        for (int m = 0; m < R; ++m) v[m] = smq[S::map2(rbase, rbase_m, m * G)];
+      }
       // twiddles w_{L r}^{q k}, k = b mod L  (kernels.py:41-72, gathered
       // from the plan table instead of rebuilt per call)
       const C* twp = tw + pass_twiddle_offset(N, R, p);
@@ -315,17 +346,45 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
       }
     } else {
       if constexpr (p > 0) seq_sync<G, SEQ>(s);  // everyone has read before we overwrite
+      constexpr bool aligned = (L == 1 && r == R);  // wbase = b*R
+      if constexpr (SPLIT) {
+        // real parts: scatter, barrier, gather the next pass's x[j + m*G];
+        // then the imaginary parts the same way (v[.].x already holds new
+        // values while v[.].y is still scattered from the old ones)
+        static_for<0, 2>([&](auto H) {
+          constexpr int h = decltype(H)::value;
+          if constexpr (h == 1) seq_sync<G, SEQ>(s);  // real parts read before the buffer is reused
 #pragma unroll
-      for (int t = 0; t < NB; ++t) {
-        const int b = j + t * G;
-        const int k = b & (L - 1);
-        const int wbase = sbase + (b - k) * r + k;
-        const int wbase_m = S::map(wbase);
-        constexpr bool aligned = (L == 1 && r == R);  // wbase = b*R
+          for (int t = 0; t < NB; ++t) {
+            const int b = j + t * G;
+            const int k = b & (L - 1);
+            const int wbase = sbase + (b - k) * r + k;
+            const int wbase_m = S::map(wbase);
 #pragma unroll
-        for (int q = 0; q < r; ++q) smq[S::map2(wbase, wbase_m, q * L, aligned)] = v[t + q * NB];
+            for (int q = 0; q < r; ++q) {
+              const C& y = v[t + q * NB];
+              sq[S::map2(wbase, wbase_m, q * L, aligned)] = h == 0 ? y.x : y.y;
+            }
+          }
+          seq_sync<G, SEQ>(s);
+#pragma unroll
+          for (int m = 0; m < R; ++m) {
+            const T x = sq[S::map2(rbase, rbase_m, m * G)];
+            if constexpr (h == 0) v[m].x = x; else v[m].y = x;
+          }
+        });
+      } else {
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          const int b = j + t * G;
+          const int k = b & (L - 1);
+          const int wbase = sbase + (b - k) * r + k;
+          const int wbase_m = S::map(wbase);
+#pragma unroll
+          for (int q = 0; q < r; ++q) smq[S::map2(wbase, wbase_m, q * L, aligned)] = v[t + q * NB];
+        }
+        seq_sync<G, SEQ>(s);
       }
-      seq_sync<G, SEQ>(s);
     }
   });
 }
@@ -399,6 +458,7 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
   constexpr int SN = S::size(N);  // smem elements per sequence
   static_assert(G >= 1 && (N % R) == 0, "geometry");
   static_assert(G <= 32 || SEQ <= 4, "named barrier ids");
+  static_assert(LOADER == 0 || LAYOUT != 3, "the split exchange region cannot stage a whole row");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* sm = reinterpret_cast<C*>(smem_raw);

@@ -24,6 +24,7 @@ std::vector<Variant> table_f64_1024(int log2n) {
           stockham_variant<double, 1024, 16, 1, 2, 0, 1>(),  // TWP 0 + bulk TMA
           stockham_variant<double, 1024, 32, 1, 2, 1, 0>(),  // R32, LDG
           stockham_variant<double, 1024, 32, 2, 2, 1, 1>(),  // R32, bulk TMA, 2 sequences per CTA
+          stockham_variant<double, 1024, 32, 1, 2, 3, 1, true>(),  // TWP 3: burst and sustained within 0.1 % of entry 0
       };
     default:
       return {};

@@ -31,6 +31,17 @@ std::vector<Variant> table_f64_2048(int log2n) {
           // conflict but needs 256 small bulk copies per row, which cut the rate
           // to 5.76 TB/s.  Kept as a tested variant (profiles/r02_wide_radix_study.txt).
           split2_variant<double, 2048, 32, 2, 1, true>(),
+          // The two below probe what limits entry 0 under the power cap -- the
+          // L1 data pipe (LSU wavefronts), not shared-memory capacity or the
+          // FP64 pipe (profiles/r02_fp64_2048_datapipe.txt):
+          // split re/im exchange (LAYOUT 3, 16 KB per sequence) + per-thread
+          // loads: 28 % fewer shared wavefronts, but the LDG data costs more
+          // data-pipe cycles than bulk copy + gather; burst -0.2 %, sustained +0.6 %
+          stockham_variant<double, 2048, 16, 1, 3, 1, 0, true>(),
+          // TWP 3 (one twiddle load per butterfly, squarings) + bulk TMA: data
+          // pipe 75.6 -> 70.4 %, sustained +1.8 %, burst equal, but 19 % more
+          // fp64 error (rel-L2 6.6e-16 vs 5.5e-16), so entry 0 stays
+          stockham_variant<double, 2048, 16, 1, 2, 3, 1, true>(),
       };
     default:
       return {};

@@ -25,8 +25,9 @@ struct Variant {
   int kernel;      // SFFT_KERNEL_*
   int r;           // elements per thread (stockham R; tile: n)
   int seq;         // sequences per CTA
-  int layout;      // smem layout (stockham): 0 xor swizzle, 1 padded
-  int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products
+  int layout;      // smem layout (stockham): 1 padded, 2 row swizzle, 3 split re/im exchange (fp64)
+  int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products,
+                   // 2 two-level split, 3 one load + squarings (sfft_kernels.cuh)
   int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA,
                    // 2 persistent CTAs with a `stages`-deep bulk TMA pipeline
   int stages;      // loader 2: shared-memory stage buffers per CTA

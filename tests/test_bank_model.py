@@ -56,6 +56,8 @@ def stockham_instructions(info, esize):
     def addr(s, e):
         if layout == 1:
             return s * region + e + e // r
+        if layout == 3:  # split exchange: 8-byte words, real then imaginary parts
+            return swz_row(s * n + e, r, 8)
         assert layout == 2
         return swz_row(s * n + e, r, esize)
 
@@ -77,6 +79,8 @@ def stockham_instructions(info, esize):
                         idx.append(addr(s, (b - k) * rad + k + q * stride))
                     out.append(idx)
         stride *= rad
+    if layout == 3:
+        out = out + out  # the same pattern for the imaginary parts
     return out
 
 
@@ -116,7 +120,7 @@ def split2_gather(info):
 def conflict_ratio(info, esize):
     if info["kernel"] == _native.SFFT_KERNEL_STOCKHAM:
         instrs = stockham_instructions(info, esize)
-        unit = esize
+        unit = 8 if info["layout"] == 3 else esize
     elif info["kernel"] == _native.SFFT_KERNEL_SPLIT2:
         instrs = split2_instructions(info, esize)
         unit = esize
@@ -169,6 +173,20 @@ def test_split2_gather_is_exactly_two_way():
                     a, b = wavefronts(idx, esize)
                     tot, ideal = tot + a, ideal + b
                 assert tot == 2 * ideal
+                seen += 1
+    assert seen >= 1
+
+
+def test_split_exchange_variant_conflict_free():
+    """LAYOUT 3 (fp64, real then imaginary parts through 8-byte words) is
+    conflict-free wherever it is compiled."""
+    lib = _native.lib()
+    seen = 0
+    for n in ALL_N:
+        for v in range(lib.sfft_num_variants(n, 1)):
+            info = _native.variant_info(n, 1, v)
+            if info["kernel"] == _native.SFFT_KERNEL_STOCKHAM and info["layout"] == 3:
+                assert conflict_ratio(info, 16) == 1.0
                 seen += 1
     assert seen >= 1
 
