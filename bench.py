@@ -565,7 +565,10 @@ def run_gpu(args, n, batch, precision, direction, workload):
             "global_batch": total_rows,
             "precision": precision,
             "direction": direction,
-            "parallelism": f"batch-sharded x{world} (independent launches, no collective)",
+            "parallelism": f"batch-sharded x{world} (independent launches, no collective)"
+                           + (" -- TEST HOOK: all ranks share one device (SFFT_BENCH_DEVICE), a code-path check; "
+                              "the ranks' kernels time-slice the GPU, so value is NOT a multi-GPU throughput"
+                              if world > 1 and "SFFT_BENCH_DEVICE" in os.environ else ""),
             "l2_policy": (f"input {batch * rb / 2**20:.0f} MiB per GPU > {l2_bytes / 2**20:.0f} MiB L2; no flush needed"
                           if batch * rb > l2_bytes else
                           f"input {batch * rb / 2**20:.0f} MiB per GPU fits the {l2_bytes / 2**20:.0f} MiB L2 "
