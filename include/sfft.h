@@ -153,8 +153,11 @@ int sfft_execute_sync_ex(sfft_plan_t plan, const void* d_in, void* d_out, int64_
 
 /* Synchronous execute on host memory: chunked H2D -> kernel -> D2H pipeline
  * over several streams (pinned memory gives full PCIe/C2C bandwidth);
- * calls up to 1 MiB take a single-stream latency path (pageable memory is
- * bounced through a pinned buffer).  The streams, device chunk buffers and
+ * calls of up to 1 MiB of output run zero-copy: one kernel launch reads and
+ * writes page-locked, host-mapped memory directly (16-byte aligned pinned
+ * user buffers in place, pageable ones through a mapped staging buffer), no
+ * copy-engine transfers (SFFT_ZERO_COPY_BYTES=0 restores the single-stream
+ * H2D/D2H path for those calls).  The streams, device chunk buffers and
  * pinned staging belong to the device, are shared by all plans on it and
  * live as long as the process; host calls on one device run one at a time.
  * Returns SFFT_ERR_DOMAIN if the input held NaN/Inf (output then undefined). */

@@ -274,3 +274,39 @@ def test_real_input_every_real_capable_variant(cuda, prec):
                 assert torch.equal(y, sf.execute(plan, xr.to(cdt))), (n, v, direction)
                 checked += 1
     assert checked >= 2 * 11
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_zero_copy_small_calls(cuda, prec):
+    """Host calls of <= 1 MiB output run the kernel on page-locked, host-mapped
+    memory (sfft_execute_host zero-copy path): pageable or pinned input and
+    output in every combination, in place on a pinned buffer, and real rows
+    -- bit-identical to the device path, at every N, from one row up to the
+    1 MiB limit and one row past it (the copy-engine path)."""
+    import itertools
+
+    esize = 8 if prec == "single" else 16
+    for p in range(1, 12):
+        n = 2**p
+        plan = sf.make_plan(n, precision=prec)
+        for rows in (1, 5, (1 << 20) // (n * esize), (1 << 20) // (n * esize) + 1):
+            x = sf.generate_batch(rows, n, seed=p + rows, precision=prec)
+            want = sf.execute(plan, torch.from_numpy(x).to(cuda)).cpu().numpy()
+            for pin_in, pin_out in itertools.product((False, True), repeat=2):
+                xi = torch.from_numpy(x.copy()).pin_memory().numpy() if pin_in else x.copy()
+                out = (torch.empty(x.shape, dtype=torch.from_numpy(x).dtype, pin_memory=True).numpy()
+                       if pin_out else np.empty_like(x))
+                got = sf.execute(plan, xi, out=out)
+                assert got is out and np.array_equal(got, want), (n, rows, pin_in, pin_out)
+                assert np.array_equal(xi, x)  # the input is never written
+            buf = torch.from_numpy(x.copy()).pin_memory().numpy()
+            sf.execute(plan, buf, out=buf)  # in place, both sides mapped
+            assert np.array_equal(buf, want), (n, rows)
+        xr = np.ascontiguousarray(x.real)
+        xr_pinned = torch.from_numpy(xr).pin_memory().numpy()
+        want_r = sf.execute(plan, xr.astype(plan.dtype))
+        assert np.array_equal(sf.execute(plan, xr_pinned), want_r)
+        bad = x.copy()
+        bad[-1, -1] = np.nan
+        with pytest.raises(sf.DomainError):
+            sf.execute(plan, torch.from_numpy(bad).pin_memory().numpy())
