@@ -165,6 +165,9 @@ constexpr int64_t kSmallCallBytes = int64_t(1) << 20;  // single-stream fast pat
 // Zero-copy latency path: calls whose output is at most this many bytes run
 // the kernel straight on pinned, mapped host staging (env
 // SFFT_ZERO_COPY_BYTES overrides, 0 disables, capped at kSmallCallBytes).
+// Not for large calls: one kernel over 512 MiB of mapped pinned rows moves
+// 39 GB/s each way against the copy engines' 45 (c2 e2e 13.8 vs 11.9 ms,
+// tools/gpu_zc_pinned_r02.sh) -- SM-initiated PCIe traffic is the slower path.
 int64_t zero_copy_bytes() {
   static const int64_t v = [] {
     int64_t b = kSmallCallBytes;  // faster than the copy engines at every size up to 1 MiB
@@ -596,6 +599,8 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
     hp.ready = true;
   }
+  const int64_t total = batch * row_bytes;
+  const int64_t total_in = batch * in_row_bytes;
   // chunks large enough for full-rate DMA, small enough to overlap copies in
   // both directions with the kernels of neighbouring chunks.
   // Staging buffers grow on demand, so small calls stay small.
@@ -619,8 +624,6 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     hp.slot_bytes = chunk_rows * row_bytes;
   }
   for (int i = 0; i < kMaxHostStreams; ++i) hp.h_flag[i] = 0;
-  const int64_t total = batch * row_bytes;
-  const int64_t total_in = batch * in_row_bytes;
 
   if (total <= zero_copy_bytes()) {
     // zero-copy latency path: the kernel reads its input from and writes its
