@@ -21,6 +21,7 @@ while it loads the data, so validation costs no extra pass over memory.
 from __future__ import annotations
 
 import ctypes
+import math
 import mmap
 import time
 from typing import NamedTuple
@@ -66,12 +67,27 @@ def _get_raw_stream_slow(device_index: int) -> int:
 _get_raw_stream = getattr(getattr(torch, "_C", None), "_cuda_getCurrentRawStream", None) or _get_raw_stream_slow
 
 
+_cuda_seen = False  # torch.cuda.is_available() costs ~2 us; once True it stays True
+
+
 def _default_device(plan: FftPlan) -> int:
+    global _cuda_seen
     if plan.device is not None:
         return plan.device
-    if torch is not None and torch.cuda.is_available():
+    if torch is not None and (_cuda_seen or torch.cuda.is_available()):
+        _cuda_seen = True
         return torch.cuda.current_device()
     return 0
+
+
+def _addr(a: np.ndarray) -> int:
+    """Data address of a C-contiguous array: the buffer protocol (~0.6 us)
+    instead of ``a.ctypes.data`` (~2 us, a fresh ctypes helper object per
+    access); read-only arrays take the slow route."""
+    try:
+        return ctypes.addressof(ctypes.c_char.from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.ctypes.data
 
 
 # ----------------------------------------------------------------- numpy path
@@ -91,7 +107,7 @@ def _prepare_host(plan: FftPlan, signal, allow_real: bool = False):
         real_t = np.float32 if plan.dtype == np.complex64 else np.float64
         return x, np.ascontiguousarray(x, dtype=real_t), rows, _native.SFFT_INPUT_REAL
     xc = np.ascontiguousarray(x, dtype=plan.dtype)
-    if xc.ctypes.data % 16:
+    if _addr(xc) % 16:
         xc = xc.copy()
     return x, xc, rows, _native.SFFT_INPUT_COMPLEX
 
@@ -106,7 +122,7 @@ def _empty_host(shape, dtype) -> np.ndarray:
     pages: the pipeline's drain copies first-touch every page, and 2 MiB
     pages cut that fault cost -- 36.8 -> 31.4 ms for a 512 MiB fresh output
     on the B200 host (tools/thp_probe.py).  Small ones use np.empty."""
-    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    nbytes = math.prod(shape) * np.dtype(dtype).itemsize
     if nbytes < _HUGE_OUTPUT_BYTES or not hasattr(mmap, "MADV_HUGEPAGE"):
         return np.empty(shape, dtype=dtype)
     m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
@@ -130,12 +146,12 @@ def _execute_host(plan: FftPlan, signal, out=None, timed: bool = False):
         or out.dtype != plan.dtype
         or out.size != xc.size
         or not out.flags.c_contiguous
-        or out.ctypes.data % 16
+        or _addr(out) % 16
     ):
         raise ShapeError("out must be a C-contiguous, 16-byte aligned array of the plan dtype and size")
     handle = plan.native_handle(_default_device(plan))
     t1 = time.perf_counter_ns()
-    _native.check(_native.lib().sfft_execute_host_ex(handle, xc.ctypes.data, out.ctypes.data, rows, kind))
+    _native.check(_native.lib().sfft_execute_host_ex(handle, _addr(xc), _addr(out), rows, kind))
     if not timed:
         return out
     t2 = time.perf_counter_ns()
