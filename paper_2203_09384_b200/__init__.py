@@ -56,7 +56,7 @@ from .bench import (
     run_benchmark,
     summarize,
 )
-from .sharding import execute_sharded, max_over_ranks, shard_bounds
+from .sharding import execute_sharded, execute_shards, gather_rows, max_over_ranks, scatter_rows, shard_bounds
 from .sigio import read_signal, write_signal
 from .oracle import dft_matrix, naive_dft, naive_dft_batch
 from .stats import (
@@ -127,6 +127,9 @@ __all__ = [
     "digit_reverse",
     "execute",
     "execute_sharded",
+    "execute_shards",
+    "gather_rows",
+    "scatter_rows",
     "execute_timed",
     "export_records",
     "export_summaries",

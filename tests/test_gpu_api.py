@@ -310,3 +310,27 @@ def test_zero_copy_small_calls(cuda, prec):
         bad[-1, -1] = np.nan
         with pytest.raises(sf.DomainError):
             sf.execute(plan, torch.from_numpy(bad).pin_memory().numpy())
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_device_resident_shards(cuda, prec):
+    """scatter_rows -> execute_shards -> gather_rows (shards stay
+    resident per device, one launch each, optional gather to one device):
+    bit-identical to one execute of the whole batch, for uneven splits and
+    more devices than rows; NaN/Inf in any shard raises DomainError."""
+    n = 512
+    plan = sf.make_plan(n, precision=prec)
+    for rows, devices in ((1001, [0, 0, 0]), (2, [0, 0, 0, 0]), (4096, [0])):
+        x = torch.from_numpy(sf.generate_batch(rows, n, seed=rows, precision=prec)).to(cuda)
+        want = sf.execute(plan, x)
+        shards = sf.scatter_rows(x, devices)
+        assert len(shards) == min(rows, len(devices))
+        outs = sf.execute_shards(plan, shards)
+        assert all(o.device == s.device for o, s in zip(outs, shards))
+        assert torch.equal(sf.gather_rows(outs, 0), want)
+        host = sf.scatter_rows(x.cpu().numpy(), devices)  # from host rows too
+        assert torch.equal(sf.gather_rows(sf.execute_shards(plan, host), 0), want)
+    bad = x.clone()
+    bad[-1, 3] = float("nan")
+    with pytest.raises(sf.DomainError):
+        sf.execute_shards(plan, sf.scatter_rows(bad, [0, 0]))
