@@ -74,7 +74,9 @@ typedef struct sfft_plan_info {
   int32_t layout;              /* stockham smem layout: 1 padded, 2 row swizzle, 3 split re/im exchange (fp64) */
   int32_t twiddle_policy;      /* 0: every twiddle loaded; 1: powers of two + products */
   int32_t loader;              /* 0: per-thread global loads; 1: one bulk TMA copy per CTA;
-                                  2: persistent CTAs, pipelined bulk TMA copies */
+                                  2: persistent CTAs, pipelined bulk TMA copies;
+                                  3: one bulk TMA copy + gathers through tensor memory;
+                                  4: as 3, the staging gather only */
   int32_t smem_carveout;       /* preferred shared-memory carveout, % of max (-1: driver default) */
   int32_t pipeline_stages;     /* loader 2: shared-memory stage buffers per CTA (else 0) */
   int32_t real_input;          /* 1: SFFT_INPUT_REAL is supported (sfft_execute_ex) */

@@ -279,16 +279,95 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
   }
 }
 
+// ------------------------------------------------ tensor memory (TMEM)
+// Shared memory is read through the LSU data pipe -- the unit that limits
+// the fp64 N=2048 kernel (profiles/r02_fp64_2048_datapipe.txt).  tcgen05.cp
+// reads shared memory through the tensor-core path instead (64 B/clk/SM,
+// overlapping LDS) into tensor memory, and tcgen05.ld brings a thread's own
+// TMEM lane into registers (252 B/clk/SM) -- neither touches the LSU pipe
+// (tools/probe/tmem_probe.cu).  With one thread per TMEM lane (128-thread
+// CTAs), a gather v[m] = buf[lane + 128 m] of 16-byte elements from a linear
+// buffer is eight 128x256b copies (no-swizzle descriptor: 8-row core matrices
+// 128 B apart, the two 16-byte K chunks 2048 B apart; layout pinned by
+// tools/probe/tmem_layout_probe.cu) plus two 32-column loads per thread.
+struct TmemGather {
+  uint32_t tmem;                // this CTA's 64 allocated columns (lane 0)
+  unsigned long long* bar;      // completion of the copies (tcgen05.commit)
+  uint32_t phase;               // next parity to wait for on `bar`
+};
+
+__device__ __forceinline__ uint64_t tmem_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SM100 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4
+  // [16,30), SBO >> 4 [32,46), version 1 [46,48), no swizzle
+  return uint64_t((saddr >> 4) & 0x3fff) | (uint64_t((lbo >> 4) & 0x3fff) << 16) |
+         (uint64_t((sbo >> 4) & 0x3fff) << 32) | (uint64_t(1) << 46);
+}
+
+// v[m] = buf[lane + 128 m], m < 16, for a linear 2048 x 16-byte buffer.  Called
+// by all 128 threads after a barrier that orders the buffer's writes (with
+// fence.proxy.async by the writers) and every earlier read of the TMEM
+// columns (tcgen05.fence::before_thread_sync by the readers).
+__device__ __forceinline__ void tmem_gather16(double2 (&v)[16], const void* buf, TmemGather& g) {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0) {
+    const uint32_t s0 = smem_u32(buf);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t d = tmem_smem_desc(s0 + k * 4096, 2048, 128);
+      asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(g.tmem + k * 8), "l"(d) : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(g.bar))
+                 : "memory");
+  }
+  mbar_wait(g.bar, g.phase);
+  g.phase ^= 1;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // two 32-column halves (8 complex doubles each), so only 32 staging
+  // registers are live next to v[]
+  const uint32_t src = g.tmem + (uint32_t(threadIdx.x & ~31) << 16);  // the warp's 32 lanes
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(src + 32 * h));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+      v[8 * h + m] = double2{__hiloint2double(int(r[4 * m + 1]), int(r[4 * m])),
+                             __hiloint2double(int(r[4 * m + 3]), int(r[4 * m + 2]))};
+  }
+  // the columns may be overwritten by the next gather once every thread has
+  // passed a barrier after this point
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// other geometries never take the TMEM path (stockham_passes' static_assert);
+// this overload only keeps its discarded branch well-formed for them
+template <typename C, int M>
+__device__ __forceinline__ void tmem_gather16(C (&)[M], const void*, TmemGather&) {}
+
 // The radix passes of one Stockham sequence, shared by both kernels below.
 // On entry v[m] = x[j + m*G] (pass-0 inputs, already validated); the
 // exchange region `smq` (per-sequence for LAYOUT 1, CTA-wide for LAYOUT 2
 // with `sbase` = s*N) is free; on exit the outputs are stored to `dst_row`
 // (nullptr: sequence past the batch, nothing stored) and the region has been
 // read for the last time by this thread.
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP>
+//
+// TMEM_LAST (fp64, G = 128, R = 16, one sequence per CTA): the exchange that
+// feeds the last pass is scattered to a linear buffer (its Stockham pattern
+// writes 8 consecutive 16-byte elements per 8-lane phase: conflict-free
+// without a swizzle) and gathered through tensor memory (tmem_gather16)
+// instead of LDS.
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, bool TMEM_LAST = false>
 __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __restrict__ smq, int sbase, int j,
                                                 int s, cx_t<T>* __restrict__ dst_row,
-                                                const cx_t<T>* __restrict__ tw) {
+                                                const cx_t<T>* __restrict__ tw,
+                                                TmemGather* tg = nullptr) {
   using C = cx_t<T>;
   using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
@@ -298,6 +377,7 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
     for (int m = 0; m < R; ++m) v[m] = cswap(v[m]);
   }
   constexpr bool SPLIT = (LAYOUT == 3);  // exchange real parts, then imaginary parts
+  static_assert(!TMEM_LAST || (sizeof(T) == 8 && G == 128 && R == 16 && SEQ == 1 && !SPLIT), "TMEM gather geometry");
   T* __restrict__ sq = reinterpret_cast<T*>(smq);
   const int rbase = sbase + j;
   const int rbase_m = S::map(rbase);
@@ -309,8 +389,8 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
     constexpr int NB = R / r;  // butterflies per thread in this pass
     if constexpr (p > 0) {
       // gather this pass's inputs x[j + m*G] from the exchange buffer (the
-      // split exchange gathered them at the end of the previous pass)
-      if constexpr (!SPLIT) {
+      // split exchange and the TMEM gather did it at the end of the previous pass)
+      if constexpr (!SPLIT && !(TMEM_LAST && p == NP - 1)) {
 #pragma unroll
         for (int m = 0; m < R; ++m) v[m] = smq[S::map2(rbase, rbase_m, m * G)];
       }
@@ -347,7 +427,20 @@ __device__ __forceinline__ void stockham_passes(cx_t<T> (&v)[R], cx_t<T>* __rest
     } else {
       if constexpr (p > 0) seq_sync<G, SEQ>(s);  // everyone has read before we overwrite
       constexpr bool aligned = (L == 1 && r == R);  // wbase = b*R
-      if constexpr (SPLIT) {
+      if constexpr (TMEM_LAST && p == NP - 2) {
+        // linear scatter, then the last pass's gather through tensor memory
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          const int b = j + t * G;
+          const int k = b & (L - 1);
+          const int wbase = sbase + (b - k) * r + k;
+#pragma unroll
+          for (int q = 0; q < r; ++q) smq[wbase + q * L] = v[t + q * NB];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS visible to tcgen05.cp
+        seq_sync<G, SEQ>(s);
+        tmem_gather16(v, smq, *tg);
+      } else if constexpr (SPLIT) {
         // real parts: scatter, barrier, gather the next pass's x[j + m*G];
         // then the imaginary parts the same way (v[.].x already holds new
         // values while v[.].y is still scattered from the old ones)
@@ -517,6 +610,72 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
                                                   s, valid ? out + seq * N : nullptr, tw);
   if (nonfinite != nullptr && valid && !in_place && j == 0 && !cx_finite(v[0]))
     recheck_row_inputs(in + seq * N, N, nonfinite);
+}
+
+// LOADER 3 (fp64 N = 2048, R = 16, 128 threads, one sequence per CTA): the
+// LOADER 1 kernel with two of its three shared-memory gathers moved to
+// tensor memory -- the row staged by the bulk copy and the exchange that
+// feeds the last pass reach registers through tcgen05.cp + tcgen05.ld, so
+// the L1 data pipe carries only the bulk-copy writes, two scatters, one
+// gather and the stores (~1300 instead of ~1930 wavefront-cycles per row).
+// The arithmetic is stockham_passes' unchanged: results are bit-identical
+// to LOADER 1's.  Real rows (RIN) are gathered with LDS (8-byte elements
+// do not fit the copy's 16-byte rows) and still take the TMEM exchange.
+// MINB: minimum resident CTAs per SM requested from ptxas (register cap);
+// XCH: also gather the last exchange through TMEM (else LDS, as LOADER 1).
+template <typename T, int N, int R, bool INV, int TWP, bool RIN = false, int MINB = 1, bool XCH = true>
+__global__ void __launch_bounds__(N / R, MINB)
+stockham_tmem_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
+                     const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  constexpr int G = N / R;
+  static_assert(sizeof(T) == 8 && G == 128 && R == 16, "TMEM gather geometry: fp64, 128 lanes, 16 elements");
+  constexpr int TMEM_COLS = 64;  // 16 complex doubles per lane
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  __shared__ __align__(8) unsigned long long bar_tma, bar_cp;
+  __shared__ uint32_t tmem_base;
+
+  const int j = threadIdx.x;
+  const long long seq = blockIdx.x;  // grid = batch: every CTA owns one valid row
+  pdl_enter();
+  if (j < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (j == 0) {
+    mbar_init(&bar_tma, 1);
+    mbar_init(&bar_cp, 1);
+    constexpr uint32_t bytes = uint32_t(N * int(sizeof(*in)));
+    mbar_expect_tx(&bar_tma, bytes);
+    bulk_g2s(sm, in + seq * N, bytes, &bar_tma);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();  // barriers initialised, TMEM address published
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  TmemGather tg{tmem_base, &bar_cp, 0};
+  mbar_wait(&bar_tma, 0);
+  C v[R];
+  if constexpr (RIN) {
+    const T* smr = reinterpret_cast<const T*>(smem_raw);
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = C{smr[j + m * G], T(0)};
+  } else {
+    tmem_gather16(v, sm, tg);  // the bulk copy's writes are async-proxy writes: no proxy fence needed
+  }
+  __syncthreads();  // staging fully read before the exchange reuses it
+  const bool in_place = static_cast<const void*>(in) == static_cast<const void*>(out);
+  if (nonfinite != nullptr && in_place) check_nonfinite<T, R>(v, nonfinite);
+  stockham_passes<T, N, R, 1, INV, 2, TWP, XCH>(v, sm, 0, j, 0, out + seq * N, tw, &tg);
+  if (nonfinite != nullptr && !in_place && j == 0 && !cx_finite(v[0])) recheck_row_inputs(in + seq * N, N, nonfinite);
+  __syncthreads();  // every lane's TMEM loads are complete (fenced in tmem_gather16)
+  if (j < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tg.tmem), "n"(TMEM_COLS) : "memory");
+  }
 }
 
 // Two-warp kernel for N = 2 * 32 * R (fp64 N = 2048 with R = 32): one level of

@@ -42,6 +42,14 @@ std::vector<Variant> table_f64_2048(int log2n) {
           // pipe 75.6 -> 70.4 %, sustained +1.8 %, burst equal, but 19 % more
           // fp64 error (rel-L2 6.6e-16 vs 5.5e-16), so entry 0 stays
           stockham_variant<double, 2048, 16, 1, 2, 3, 1, true>(),
+          // bulk TMA + tensor-memory gathers: entry 0's kernel with the staging
+          // gather and the last exchange's gather on tcgen05.cp/ld (loader 3),
+          // or the staging gather only (loader 4).  The L1 data pipe drops from
+          // 75.6 to 43 % of peak, but each 32 KB copy into TMEM takes ~512
+          // cycles (64 B/clk) on the CTA's critical path: burst 5.55 / 6.14 vs
+          // 6.96 TB/s, sustained 5.20 / 5.41 vs 5.81 (profiles/r02_fp64_2048_datapipe.txt)
+          tmem_variant<double, 2048, 16, 1, true>(),
+          tmem_variant<double, 2048, 16, 1, true, 1, false>(),
       };
     default:
       return {};

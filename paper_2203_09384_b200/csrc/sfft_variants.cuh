@@ -29,7 +29,9 @@ struct Variant {
   int twp;         // twiddle policy (stockham): 0 all loaded, 1 powers of two + products,
                    // 2 two-level split, 3 one load + squarings (sfft_kernels.cuh)
   int loader;      // input path (stockham): 0 per-thread LDG, 1 one bulk TMA copy per CTA,
-                   // 2 persistent CTAs with a `stages`-deep bulk TMA pipeline
+                   // 2 persistent CTAs with a `stages`-deep bulk TMA pipeline,
+                   // 3 bulk TMA + gathers through tensor memory (fp64 N=2048),
+                   // 4 as 3 but only the staging gather through tensor memory
   int stages;      // loader 2: shared-memory stage buffers per CTA
   int carveout;    // preferred shared-memory carveout, % of max (-1: driver default)
   int threads;     // threads per CTA
@@ -220,6 +222,43 @@ Variant pipe_variant() {
   v.launch[1] = &launch_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
   v.prepare[0] = &prepare_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
   v.prepare[1] = &prepare_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
+  return v;
+}
+
+// bulk TMA + tensor-memory gathers (sfft_kernels.cuh: stockham_tmem_kernel, loader 3)
+template <typename T, int N, int R, bool INV, int TWP, bool RIN, int MINB, bool XCH>
+cudaError_t launch_stockham_tmem(const void* in, void* out, const void* tw, long long batch, int* flag,
+                                 cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
+  return launch_pdl(pdl, sfft::stockham_tmem_kernel<T, N, R, INV, TWP, RIN, MINB, XCH>, batch, N / R,
+                    N * int(sizeof(C)), st, static_cast<const In*>(in), static_cast<C*>(out),
+                    static_cast<const C*>(tw), batch, flag);
+}
+template <typename T, int N, int R, bool INV, int TWP, bool RIN, int MINB, bool XCH>
+cudaError_t prepare_stockham_tmem(int carveout) {
+  const auto k = sfft::stockham_tmem_kernel<T, N, R, INV, TWP, RIN, MINB, XCH>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, N * int(sizeof(sfft::cx_t<T>)));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+template <typename T, int N, int R, int TWP, bool REAL = false, int MINB = 1, bool XCH = true>
+Variant tmem_variant() {
+  Variant v = stockham_variant<T, N, R, 1, 2, TWP, 1>();
+  v.loader = XCH ? 3 : 4;
+  v.carveout = -1;  // the bulk copy lands in shared memory
+  v.launch[0] = &launch_stockham_tmem<T, N, R, false, TWP, false, MINB, XCH>;
+  v.launch[1] = &launch_stockham_tmem<T, N, R, true, TWP, false, MINB, XCH>;
+  v.prepare[0] = &prepare_stockham_tmem<T, N, R, false, TWP, false, MINB, XCH>;
+  v.prepare[1] = &prepare_stockham_tmem<T, N, R, true, TWP, false, MINB, XCH>;
+  v.launch_real[0] = v.launch_real[1] = nullptr;
+  v.prepare_real[0] = v.prepare_real[1] = nullptr;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_stockham_tmem<T, N, R, false, TWP, true, MINB, XCH>;
+    v.launch_real[1] = &launch_stockham_tmem<T, N, R, true, TWP, true, MINB, XCH>;
+    v.prepare_real[0] = &prepare_stockham_tmem<T, N, R, false, TWP, true, MINB, XCH>;
+    v.prepare_real[1] = &prepare_stockham_tmem<T, N, R, true, TWP, true, MINB, XCH>;
+  }
   return v;
 }
 

@@ -62,21 +62,27 @@ def stockham_instructions(info, esize):
         return swz_row(s * n + e, r, esize)
 
     lanes = [(lane // g, lane % g) if g < 32 else (0, lane) for lane in range(32)]
+    # loader 3: the exchange feeding the last pass is scattered linearly and
+    # gathered through tensor memory (tcgen05.cp), not with LDS
+    tmem_last = info["loader"] == 3
+    last = len(radices) - 1
     out = []
     stride = 1
     for pi, rad in enumerate(radices):
         nb = r // rad
-        if pi > 0:  # gather x[j + m*G]
+        if pi > 0 and not (tmem_last and pi == last):  # gather x[j + m*G]
             for mm in range(r):
                 out.append([addr(s, j + mm * g) for s, j in lanes])
-        if pi < len(radices) - 1:  # scatter to the Stockham destination
+        if pi < last:  # scatter to the Stockham destination
+            linear = tmem_last and pi == last - 1
             for t in range(nb):
                 for q in range(rad):
                     idx = []
                     for s, j in lanes:
                         b = j + t * g
                         k = b % stride
-                        idx.append(addr(s, (b - k) * rad + k + q * stride))
+                        e = (b - k) * rad + k + q * stride
+                        idx.append(s * n + e if linear else addr(s, e))
                     out.append(idx)
         stride *= rad
     if layout == 3:
@@ -188,6 +194,21 @@ def test_split_exchange_variant_conflict_free():
             if info["kernel"] == _native.SFFT_KERNEL_STOCKHAM and info["layout"] == 3:
                 assert conflict_ratio(info, 16) == 1.0
                 seen += 1
+    assert seen >= 1
+
+
+def test_tmem_gather_variant_conflict_free():
+    """Loader 3 (fp64 N=2048: the last exchange scattered to a linear buffer
+    and gathered through tensor memory): the linear scatter of the Stockham
+    pattern writes 8 consecutive 16-byte elements per phase -- conflict-free
+    without a swizzle -- and the remaining LDS/STS stay conflict-free."""
+    lib = _native.lib()
+    seen = 0
+    for v in range(lib.sfft_num_variants(2048, 1)):
+        info = _native.variant_info(2048, 1, v)
+        if info["loader"] == 3:
+            assert conflict_ratio(info, 16) == 1.0
+            seen += 1
     assert seen >= 1
 
 
