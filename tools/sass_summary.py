@@ -9,6 +9,7 @@ Blackwell-native code paths:
   ``DADD`` / ``DMUL`` / ``DFMA``;
 * global and shared access widths: ``LDG``/``STG``/``LDS``/``STS`` by width
   (32 / 64 / 128 bit), ``LDGSTS`` (cp.async), ``BAR``;
+* tensor memory: ``UTCCP`` (tcgen05.cp smem -> TMEM), ``LDTM`` (tcgen05.ld);
 * total static instruction count.
 
 Default kernels (variant 0 of each length / precision / direction / input
@@ -30,7 +31,7 @@ sys.path.insert(0, ROOT)
 LIB = os.path.join(ROOT, "paper_2203_09384_b200", "_lib", "libsfft.so")
 
 OPS = ("UBLKCP", "SYNCS", "FADD2", "FMUL2", "FFMA2", "FADD", "FMUL", "FFMA", "DADD", "DMUL", "DFMA", "LDGSTS",
-       "BAR", "SHFL")
+       "BAR", "SHFL", "UTCCP", "LDTM")
 
 
 def demangle(names):
@@ -111,6 +112,11 @@ def classify(demangled: str, sigs):
     if m:
         return (f"split2 {m.group(1)} N={m.group(2)} R={m.group(3)} {'inv' if m.group(4) == '1' else 'fwd'} "
                 f"layout={m.group(5)} twp={m.group(6)}{' real-in' if m.group(7) == '1' else ''}"), False
+    m = re.search(r"sfft::stockham_tmem_kernel<(float|double), (\d+), (\d+), ([01]), (\d), ([01]), (\d), ([01])>", d)
+    if m:
+        return (f"stockham_tmem {m.group(1)} N={m.group(2)} R={m.group(3)} {'inv' if m.group(4) == '1' else 'fwd'} "
+                f"twp={m.group(5)} minb={m.group(7)} loader={'3' if m.group(8) == '1' else '4'}"
+                f"{' real-in' if m.group(6) == '1' else ''}"), False
     m = re.search(r"sfft::stockham_pipe_kernel<(float|double), (\d+), (\d+), (\d+), ([01])", d)
     if m:
         return (f"stockham_pipe {m.group(1)} N={m.group(2)} R={m.group(3)} seq={m.group(4)} "
@@ -129,7 +135,7 @@ def main():
     sigs = default_signatures()
     cols = ["total", "UBLKCP", "SYNCS", "FFMA2", "FADD2", "FMUL2", "FFMA", "FADD", "FMUL", "DADD", "DMUL", "DFMA",
             "LDG.32", "LDG.64", "LDG.128", "LDGSTS", "STG.32", "STG.64", "STG.128", "LDS.64", "LDS.128", "STS.64",
-            "STS.128", "BAR"]
+            "STS.128", "BAR", "UTCCP", "LDTM"]
     rows = []
     for mangled, c in kernels.items():
         label, is_default = classify(names[mangled], sigs)
