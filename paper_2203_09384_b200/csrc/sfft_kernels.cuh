@@ -17,6 +17,10 @@
 // * split2_kernel    (tested variant, fp64 N = 2048): two one-warp N/2
 //   transforms of the polyphase halves plus a radix-2 combine.
 //
+// * stockham_tmem_kernel (tested variant, fp64 N = 2048): the bulk-TMA
+//   Stockham kernel with shared-memory gathers routed through tensor memory
+//   (tcgen05.cp + tcgen05.ld) to take them off the L1 data pipe.
+//
 // * tile_kernel      (N <= 32 fp32, N <= 16 fp64)
 //   One thread owns whole sequences.  A warp stages a contiguous tile of
 //   32*SPT sequences into swizzled shared memory with 16-byte cp.async
