@@ -7,6 +7,7 @@
 //   mode 2: modes 0 and 1 together (warps 1-3 LDS, warp 0 lane 0 cp)
 //   mode 3: tcgen05.ld 32x32b.x16 TMEM -> registers, 4 warps
 //   mode 4: modes 0 (warps 0-3 LDS) and 3 interleaved per warp
+//   mode 5: mode 1's copies issued by lane 0 of all four warps (a quarter each)
 // One CTA of 128 threads per SM, 64 KB of shared memory, all 512 TMEM columns.
 // Cycles from clock64() of the slowest CTA; run under ncu for the pipe counters.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tmem_probe tmem_probe.cu
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(128, 1) probe(float* out, long long* cycles) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(MODE == 5 ? 4 : 1));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -52,11 +53,12 @@ __global__ void __launch_bounds__(128, 1) probe(float* out, long long* cycles) {
 
   const long long t0 = clock64();
   const bool do_lds = MODE == 0 || MODE == 4 || (MODE == 2 && warp > 0);
-  const bool do_cp = (MODE == 1 || MODE == 2) && tid == 0;
+  const bool do_cp = ((MODE == 1 || MODE == 2) && tid == 0) || (MODE == 5 && (tid & 31) == 0);
+  const int cp_iters = MODE == 5 ? ITERS / 4 : ITERS;
   const bool do_ld = MODE == 3 || MODE == 4;
   if (do_cp) {
     const uint32_t s0 = smem_u32(smem);
-    for (int i = 0; i < ITERS; ++i) {
+    for (int i = warp * cp_iters; i < (warp + 1) * cp_iters; ++i) {
       // 128 rows x 32 B = 4 KB per copy, rotating over the 64 KB buffer and 8 column groups
       const uint64_t d = smem_desc(s0 + (i & 15) * 4096, 128, 256);
       const uint32_t dst = tmem + ((i & 7) * 8);  // 8 columns (32 B) per lane
@@ -127,11 +129,13 @@ int main() {
   const double lds_bytes = 128.0 * 16 * ITERS;        // per SM
   const double cp_bytes = 4096.0 * ITERS;              // per SM
   const double ld_bytes = 128.0 * 16 * 4 * ITERS;      // 4 warps x 32 lanes x 16 words
-  const double c0 = run<0>(sms), c1 = run<1>(sms), c2 = run<2>(sms), c3 = run<3>(sms), c4 = run<4>(sms);
+  const double c0 = run<0>(sms), c1 = run<1>(sms), c2 = run<2>(sms), c3 = run<3>(sms), c4 = run<4>(sms),
+               c5 = run<5>(sms);
   printf("mode 0 LDS only      : %9.0f cycles, %6.1f B/clk/SM\n", c0, lds_bytes / c0);
   printf("mode 1 tcgen05.cp    : %9.0f cycles, %6.1f B/clk/SM\n", c1, cp_bytes / c1);
   printf("mode 2 cp + LDS(3w)  : %9.0f cycles (LDS alone 3 warps ~ %.0f, cp alone %.0f)\n", c2, c0 * 0.75, c1);
   printf("mode 3 tcgen05.ld    : %9.0f cycles, %6.1f B/clk/SM\n", c3, ld_bytes / c3);
   printf("mode 4 ld + LDS      : %9.0f cycles (sum %.0f, max %.0f)\n", c4, c0 + c3, c0 > c3 ? c0 : c3);
+  printf("mode 5 cp, 4 issuers : %9.0f cycles, %6.1f B/clk/SM\n", c5, cp_bytes / c5);
   return 0;
 }
