@@ -603,26 +603,31 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   const int64_t total_in = batch * in_row_bytes;
   // chunks large enough for full-rate DMA, small enough to overlap copies in
   // both directions with the kernels of neighbouring chunks.
-  // Staging buffers grow on demand, so small calls stay small.
+  // Staging buffers grow on demand, so small calls stay small (and
+  // zero-copy calls allocate none).
   const int64_t chunk_bytes = host_shape().chunk_bytes;
   const int64_t max_chunk_rows = chunk_bytes / row_bytes > 0 ? chunk_bytes / row_bytes : 1;
   const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
   const int64_t chunk_rows = want_rows;  // rows per pipeline chunk of this call
-  if (chunk_rows * row_bytes > hp.slot_bytes) {  // capacity in bytes: plans of any N share the slots
-    for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) cudaStreamSynchronize(st);
-    for (int i = 0; i < hp.nslots; ++i) {
-      cudaFree(hp.d_in[i]);
-      cudaFree(hp.d_out[i]);
-      hp.d_in[i] = hp.d_out[i] = nullptr;
+  auto ensure_slots = [&]() -> cudaError_t {
+    if (chunk_rows * row_bytes > hp.slot_bytes) {  // capacity in bytes: plans of any N share the slots
+      for (cudaStream_t st : {hp.st_h2d, hp.st_kernel, hp.st_d2h}) cudaStreamSynchronize(st);
+      for (int i = 0; i < hp.nslots; ++i) {
+        cudaFree(hp.d_in[i]);
+        cudaFree(hp.d_out[i]);
+        hp.d_in[i] = hp.d_out[i] = nullptr;
+      }
+      hp.slot_bytes = 0;
+      cudaError_t err = cudaSuccess;
+      for (int i = 0; i < hp.nslots && err == cudaSuccess; ++i) {
+        err = cudaMalloc(&hp.d_in[i], chunk_rows * row_bytes);
+        if (err == cudaSuccess) err = cudaMalloc(&hp.d_out[i], chunk_rows * row_bytes);
+      }
+      if (err != cudaSuccess) return err;
+      hp.slot_bytes = chunk_rows * row_bytes;
     }
-    hp.slot_bytes = 0;
-    for (int i = 0; i < hp.nslots && e == cudaSuccess; ++i) {
-      e = cudaMalloc(&hp.d_in[i], chunk_rows * row_bytes);
-      if (e == cudaSuccess) e = cudaMalloc(&hp.d_out[i], chunk_rows * row_bytes);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
-    hp.slot_bytes = chunk_rows * row_bytes;
-  }
+    return cudaSuccess;
+  };
   for (int i = 0; i < kMaxHostStreams; ++i) hp.h_flag[i] = 0;
 
   if (total <= zero_copy_bytes()) {
@@ -657,6 +662,8 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   } else if (total <= kSmallCallBytes) {
     // latency path: one stream; pageable user memory goes through a pinned
     // bounce buffer (a host memcpy is cheaper than the driver's staging)
+    e = ensure_slots();
+    if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
     if (!pinned && hp.h_stage == nullptr) {
       e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_stage), 2 * kSmallCallBytes, cudaHostAllocPortable);
@@ -677,6 +684,8 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
     if (!pinned) std::memcpy(h_out, dst, size_t(total));
   } else {
+    e = ensure_slots();
+    if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
     // Three engines, one stream each -- H2D copies, kernels, D2H copies --
     // with chunk k in device slot k % S.  Per slot:
     //   H2D(k)    waits kernel(k-S)  (d_in free)
