@@ -53,6 +53,7 @@ extern "C" {
 #define SFFT_KERNEL_STOCKHAM 0 /* G=n/R threads per sequence, smem exchange */
 #define SFFT_KERNEL_TILE 1     /* thread per sequence, warp-staged tile     */
 #define SFFT_KERNEL_SPLIT2 2   /* two one-warp half transforms + radix-2    */
+#define SFFT_KERNEL_FOURSTEP 3 /* 32 x 64 four-step, shuffle radix-2, fp64 N=2048 */
 
 typedef struct sfft_plan* sfft_plan_t;
 

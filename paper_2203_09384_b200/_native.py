@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libsfft.so")
 
 SFFT_SINGLE, SFFT_DOUBLE = 0, 1
 SFFT_FORWARD, SFFT_INVERSE = 0, 1
-SFFT_KERNEL_STOCKHAM, SFFT_KERNEL_TILE, SFFT_KERNEL_SPLIT2 = 0, 1, 2
+SFFT_KERNEL_STOCKHAM, SFFT_KERNEL_TILE, SFFT_KERNEL_SPLIT2, SFFT_KERNEL_FOURSTEP = 0, 1, 2, 3
 SFFT_INPUT_COMPLEX, SFFT_INPUT_REAL = 0, 1
 
 #: every symbol include/sfft.h declares (tests check the .so exports them all)

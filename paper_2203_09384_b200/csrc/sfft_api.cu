@@ -359,7 +359,12 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
 
   // per-pass table: pass p >= 1, entry [(q-1)*L + k] = w_{L r}^{q k} = base[(n/(L r)) q k]
   std::vector<int> tidx;
-  if (p->v->kernel != SFFT_KERNEL_TILE) {  // stockham and split2: per-pass tables
+  if (p->v->kernel == SFFT_KERNEL_FOURSTEP) {
+    // fourstep_kernel's table: tw[c * 32 + n1] = W_n^(n1 * pw[c])
+    static constexpr int pw[12] = {1, 2, 3, 4, 0, 8, 16, 24, 32, 40, 48, 56};
+    for (int c = 0; c < 12; ++c)
+      for (int n1 = 0; n1 < 32; ++n1) tidx.push_back((n1 * pw[c]) % n);
+  } else if (p->v->kernel != SFFT_KERNEL_TILE) {  // stockham and split2: per-pass tables
     int L = p->v->radices[0];
     for (int pass = 1; pass < p->v->passes; ++pass) {
       const int r = p->v->radices[pass];

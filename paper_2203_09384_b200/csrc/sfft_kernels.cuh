@@ -17,6 +17,9 @@
 // * split2_kernel    (tested variant, fp64 N = 2048): two one-warp N/2
 //   transforms of the polyphase halves plus a radix-2 combine.
 //
+// * fourstep_kernel  (tested variant, fp64 N = 2048): 32 x 64 four-step with
+//   one shared-memory exchange and three radix-2 levels through warp shuffles.
+//
 // * stockham_tmem_kernel (tested variant, fp64 N = 2048): the bulk-TMA
 //   Stockham kernel with shared-memory gathers routed through tensor memory
 //   (tcgen05.cp + tcgen05.ld) to take them off the L1 data pipe.
@@ -788,6 +791,206 @@ split2_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T
 #pragma unroll
     for (int m = 0; m < HR; ++m) combine(xs[(HR + m) * 32 + j], v[HR + m], j + (HR + m) * G);
   }
+}
+
+// Four-step kernel for fp64 N = 2048 = 32 x 64 with ONE shared-memory
+// exchange per row (the R16 default has two): 128 threads, one sequence per
+// CTA, 16 complex doubles per thread.  With n = n1 + 32 n2, k = k2 + 64 k1,
+//   X[k2 + 64 k1] = sum_n1 W32^(n1 k1) W2048^(n1 k2) sum_n2 x[n1 + 32 n2] W64^(n2 k2).
+// Step A, the 32 length-64 DFTs over n2, each on a lane quad (c0, c1) =
+//   (lane bit 3, lane bit 4): lane c = c0 + 2 c1 takes n2 = 4a + c, a
+//   radix-16 DFT in registers, then two radix-2 levels across the quad
+//   (lane ^ 16, then lane ^ 8) through __shfl_xor.
+// Step B, the twiddles W2048^(n1 k2): 6 table loads per thread, the other
+//   powers by one or two products (as TWP 2).
+// Step C, one swizzled shared-memory transpose to (k2, d) per thread, the 32
+//   length-32 DFTs over n1 = 2b + d as a radix-16 DFT in registers and one
+//   radix-2 level across lane ^ 16, and coalesced stores.
+// A shuffle moves each 4-byte word once (one L1 data-pipe cycle per 128 B);
+// a shared-memory exchange writes and reads it (two).  L1 data pipe per row:
+// gather 256 + exchange 512 + shuffles 384 + stores 256 + twiddles ~48
+// wavefronts, against ~1950 for the R16 default (gather, two exchanges,
+// stores, twiddles, bulk-copy collisions) -- the unit that bounds that kernel
+// under the power cap (profiles/r02_fp64_2048_datapipe.txt).  Conflict-free
+// (tests/test_bank_model.py: fourstep_instructions).
+// Measured (profiles/r02_fourstep_study.txt): the data pipe drops to 57 %,
+// but the operand selects make it issue-heavier (49 vs 33 % issue active)
+// and the per-row critical path longer; with 4-5 rows in flight per SM it
+// reaches 0.94-0.95x the copy at burst -- a tested variant, not the default.
+// Every radix-2 level across a lane pair has both lanes send registers
+// 8..15: the upper lane's inputs are pre-modulated by (-1)^(input index)
+// (and, for c0 = c1 = 1, negated -- a half-swap of its level-2 operands), which
+// rotates its radix-16 outputs by 8, so no lane needs a per-lane register
+// choice to send; each lane then picks (z0, z1) from (own, received) with one
+// select, and the level's twiddle W^k for its own k.  Table (plan-built,
+// tw[c * 32 + n1], w = W2048^n1): c = 0..3 w^1..w^4; c = 4..11 w^(8 j), j = 0..7.
+template <typename C>
+__device__ __forceinline__ C shfl_xor_c(C v, int m) {
+  return C{__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
+}
+// One radix-2 level across lanes (l, l ^ M) on 2 x 8 registers: on entry
+// the lower lane (upper = false) holds A[k] in v[k] and the upper lane holds
+// B[(k + 8) mod 16] in v[k] (pre-rotated); the level computes, for its own
+// k = i + 8 upper, v[i] = A[k] + w_k B[k] and v[8 + i] = A[k] - w_k B[k] with
+// w_k = W_L^(i + J) * (-i)^upper, J = 0 or JSEL (runtime `jsel`).
+template <int M, int L, int JSEL, typename C>
+__device__ __forceinline__ void pair_level(C (&v)[16], bool upper, bool jsel) {
+  using T = decltype(v[0].x);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[8 + i] = shfl_xor_c(v[8 + i], M);
+  static_for<0, 8>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    const C own = v[i];
+    const C got = v[8 + i];
+    const C z0 = upper ? got : own;
+    const C z1 = upper ? own : got;
+    C t;
+    if constexpr (JSEL == 0) {
+      t = twiddle_const<i, L>(z1);
+    } else {
+      constexpr int j0 = i * (64 / L), j1 = (i + JSEL) * (64 / L);
+      const T c = jsel ? T(cos64(j1)) : T(cos64(j0));
+      const T s = jsel ? T(-sin64(j1)) : T(-sin64(j0));
+      t = cmul(z1, C{c, s});
+    }
+    t = upper ? mul_minus_i(t) : t;
+    v[i] = cadd(z0, t);
+    v[8 + i] = csub(z0, t);
+  });
+}
+__device__ __forceinline__ double flip_sign(double x, int sign_hi) {
+  return __hiloint2double(__double2hiint(x) ^ sign_hi, __double2loint(x));
+}
+
+template <typename T, bool INV, bool RIN = false, int MINB = 5>
+__global__ void __launch_bounds__(128, MINB)
+fourstep_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
+                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  using C = cx_t<T>;
+  constexpr int N = 2048;
+  constexpr int R = 16;
+  static_assert(sizeof(T) == 8, "fp64 geometry (128 threads x 16 complex doubles)");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  __shared__ __align__(8) unsigned long long bar;
+
+  const int tid = threadIdx.x;
+  const int w = tid >> 5;
+  const int lane = tid & 31;
+  const bool c0 = (lane >> 3) & 1;
+  const bool c1 = (lane >> 4) & 1;
+  const int n1 = (lane & 7) + 8 * w;
+  const long long seq = blockIdx.x;  // one sequence per CTA: every CTA is full
+  pdl_enter();
+
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    constexpr uint32_t bytes = uint32_t(N * int(sizeof(*in)));
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(sm, in + seq * N, bytes, &bar);
+  }
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+
+  // v[a] = x[n1 + 32 (4 a + c)]: 8-lane phases read 128 contiguous bytes
+  C v[R];
+  const int g0 = n1 + 32 * (int(c0) + 2 * int(c1));
+  if constexpr (RIN) {
+    const T* smr = reinterpret_cast<const T*>(smem_raw);
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = C{smr[g0 + 128 * a], T(0)};
+  } else {
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = sm[g0 + 128 * a];
+  }
+  __syncthreads();  // staging fully read before the exchange reuses it
+  const bool in_place = static_cast<const void*>(in) == static_cast<const void*>(out);
+  if (nonfinite != nullptr && in_place) check_nonfinite<T, R>(v, nonfinite);
+  if constexpr (INV) {
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = cswap(v[a]);
+  }
+
+  // ---- step A.  Upper lanes of level 1 (c1): (-1)^a rotates their outputs
+  // by 8; lane (1, 1) also negates (swaps the halves its level-2 operands
+  // land in, so level 2's upper lanes send the right half too).
+  {
+    const int s_odd = int(c1) << 31;
+    const int s_all = int(c0 && c1) << 31;
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int sg = (a & 1) ? (s_odd ^ s_all) : s_all;
+      v[a].x = flip_sign(v[a].x, sg);
+      v[a].y = flip_sign(v[a].y, sg);
+    }
+  }
+  dft_regs<R>(v);  // Z_c[k'] (rotated by 8 on c1 lanes)
+  // level 1 (n2 bit 1, lanes ^ 16): V_c0[k' + 16 h] at v[8 h + i], k' = i + 8 c1
+  pair_level<16, 32, 0>(v, c1, false);
+  // level 2 (n2 bit 0, lanes ^ 8): Y[k2] at v[8 h + i], k2 = i + 8 c1 + 16 c0 + 32 h
+  pair_level<8, 64, 8>(v, c0, c1);
+
+  // ---- step B.  v[8 h + i] *= w^(8 (c1 + 2 c0) + 32 h) w^i, w = W2048^n1
+  {
+    const C* tn = tw + n1;
+    C wp[8];
+#pragma unroll
+    for (int i = 1; i <= 4; ++i) wp[i] = __ldg(tn + (i - 1) * 32);
+#pragma unroll
+    for (int i = 5; i < 8; ++i) wp[i] = cmul(wp[4], wp[i - 4]);
+    const int j = int(c1) + 2 * int(c0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const C eh = __ldg(tn + (4 + j + 4 * h) * 32);
+      v[8 * h] = cmul(v[8 * h], eh);
+#pragma unroll
+      for (int i = 1; i < 8; ++i) v[8 * h + i] = cmul(v[8 * h + i], cmul(eh, wp[i]));
+    }
+  }
+
+  // ---- step C.  Transpose: slot(n1, k2) = 64 n1 + (k2 ^ (n1 & 7)) (8-lane
+  // phases: 8 consecutive n1 on write, 8 consecutive k2 on read).
+  {
+    const int x = n1 & 7;
+    C* wrow = sm + 64 * n1 + 8 * int(c1) + 16 * int(c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      wrow[i ^ x] = v[i];
+      wrow[32 + (i ^ x)] = v[8 + i];
+    }
+  }
+  __syncthreads();
+  // thread (k2, d): k2 = (lane & 15) + 16 w, d = lane bit 4; v[b] = Y'[2 b + d][k2]
+  const int k2 = (lane & 15) + 16 * w;
+  const bool d = c1;
+  {
+    const C* rrow = sm + 64 * int(d);
+    int kx[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) kx[q] = k2 ^ (2 * q + int(d));
+    const int s_odd = int(d) << 31;  // (-1)^b on the upper lanes: outputs rotated by 8
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      C y = rrow[128 * b + kx[b & 3]];
+      if (b & 1) y = C{flip_sign(y.x, s_odd), flip_sign(y.y, s_odd)};
+      v[b] = y;
+    }
+  }
+  dft_regs<R>(v);
+  // n1 bit 0 (lanes ^ 16): X[k2 + 64 (k1' + 16 q)] at v[8 q + i], k1' = i + 8 d
+  pair_level<16, 32, 0>(v, d, false);
+
+  C* dst = out + seq * N + k2 + 512 * int(d);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    C y = v[r];
+    if constexpr (INV) y = cscale(cswap(y), T(1) / T(N));  // exact: N = 2^k
+    st_stream(dst + 64 * (r & 7) + 1024 * (r >> 3), y);
+  }
+  // X[0] (thread 0, v[0]): the out-of-place NaN/Inf check (see recheck_row_inputs)
+  if (nonfinite != nullptr && !in_place && tid == 0 && !cx_finite(v[0]))
+    recheck_row_inputs(in + seq * N, N, nonfinite);
 }
 
 // Persistent, pipelined variant: a grid of (SMs x resident CTAs) walks the

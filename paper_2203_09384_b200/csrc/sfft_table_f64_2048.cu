@@ -50,6 +50,15 @@ std::vector<Variant> table_f64_2048(int log2n) {
           // 6.96 TB/s, sustained 5.20 / 5.41 vs 5.81 (profiles/r02_fp64_2048_datapipe.txt)
           tmem_variant<double, 2048, 16, 1, true>(),
           tmem_variant<double, 2048, 16, 1, true, 1, false>(),
+          // four-step 32 x 64 (fourstep_kernel): one shared-memory exchange per
+          // row, three radix-2 levels through warp shuffles.  The L1 data pipe
+          // drops from 74 to 57 % of peak, but choosing each lane's butterfly
+          // operands costs ~300 selects per thread (issue 33 -> 49 %), the row's
+          // critical path grows, and with 4-5 rows in flight per SM that is the
+          // rate: burst 0.94-0.95x copy, sustained 5.13-5.18 vs 5.73 TB/s for
+          // entry 0 (profiles/r02_fourstep_study.txt).  A 64-thread form (32
+          // elements per thread, one shuffle level) was latency-bound too (0.94x).
+          fourstep_variant<double, true, 4>(),
       };
     default:
       return {};

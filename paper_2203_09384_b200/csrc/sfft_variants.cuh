@@ -309,6 +309,55 @@ Variant split2_variant() {
   return v;
 }
 
+// fp64 N = 2048 four-step kernel (sfft_kernels.cuh: fourstep_kernel): four
+// warps per sequence, one exchange, three radix-2 levels through warp shuffles
+template <typename T, bool INV, bool RIN, int MINB>
+cudaError_t launch_fourstep(const void* in, void* out, const void* tw, long long batch, int* flag,
+                            cudaStream_t st, bool pdl) {
+  using C = sfft::cx_t<T>;
+  using In = std::conditional_t<RIN, T, C>;
+  return launch_pdl(pdl, sfft::fourstep_kernel<T, INV, RIN, MINB>, batch, 128, 2048 * int(sizeof(C)), st,
+                    static_cast<const In*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
+}
+template <typename T, bool INV, bool RIN, int MINB>
+cudaError_t prepare_fourstep(int carveout) {
+  const auto k = sfft::fourstep_kernel<T, INV, RIN, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * int(sizeof(sfft::cx_t<T>)));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return e;
+}
+// Steps: radix 64 (over n2) then radix 32 (over n1); the twiddle table is the
+// kernel's own (12 powers of W2048^n1 per n1, built by sfft_plan_create).
+constexpr int kFourstepTwiddleElems = 12 * 32;
+template <typename T, bool REAL = false, int MINB = 5>
+Variant fourstep_variant() {
+  Variant v{};
+  v.kernel = SFFT_KERNEL_FOURSTEP;
+  v.r = 16;
+  v.seq = 1;
+  v.layout = 0;
+  v.twp = 2;
+  v.loader = 1;
+  v.carveout = -1;  // the bulk copy lands in shared memory
+  v.threads = 128;
+  v.smem = 2048 * int(sizeof(sfft::cx_t<T>));
+  v.passes = 2;
+  v.radices[0] = 64;
+  v.radices[1] = 32;
+  v.tw_len = kFourstepTwiddleElems;
+  v.launch[0] = &launch_fourstep<T, false, false, MINB>;
+  v.launch[1] = &launch_fourstep<T, true, false, MINB>;
+  v.prepare[0] = &prepare_fourstep<T, false, false, MINB>;
+  v.prepare[1] = &prepare_fourstep<T, true, false, MINB>;
+  if constexpr (REAL) {
+    v.launch_real[0] = &launch_fourstep<T, false, true, MINB>;
+    v.launch_real[1] = &launch_fourstep<T, true, true, MINB>;
+    v.prepare_real[0] = &prepare_fourstep<T, false, true, MINB>;
+    v.prepare_real[1] = &prepare_fourstep<T, true, true, MINB>;
+  }
+  return v;
+}
+
 template <typename T, int N, int SPT, int W, bool REAL = false>
 Variant tile_variant() {
   Variant v{};

@@ -123,8 +123,31 @@ def split2_gather(info):
     return [[2 * (lane + 32 * m) + w for lane in range(32)] for w in (0, 1) for m in range(r)]
 
 
+def fourstep_instructions(info):
+    """sfft::fourstep_kernel (fp64 N = 2048, 128 threads): the staging gather
+    v[a] = x[n1 + 32 (4 a + c0 + 2 c1)], the transpose write slot(n1, k2) =
+    64 n1 + (k2 ^ (n1 & 7)) for k2 = i + 8 c1 + 16 c0 + 32 h, and its read by
+    thread (k2, d) of n1 = 2 b + d.  Lane l of warp w: c0 = bit 3, c1 = bit 4,
+    n1 = (l & 7) + 8 w; after the transpose k2 = (l & 15) + 16 w, d = bit 4."""
+    out = []
+    for w in range(4):
+        quad = [((l >> 3) & 1, (l >> 4) & 1, (l & 7) + 8 * w) for l in range(32)]
+        for a in range(16):
+            out.append([n1 + 32 * (c0 + 2 * c1) + 128 * a for c0, c1, n1 in quad])
+        for h in (0, 1):
+            for i in range(8):
+                out.append([64 * n1 + ((i + 8 * c1 + 16 * c0 + 32 * h) ^ (n1 & 7)) for c0, c1, n1 in quad])
+        pairs = [((l & 15) + 16 * w, (l >> 4) & 1) for l in range(32)]
+        for b in range(16):
+            out.append([64 * (2 * b + d) + (k2 ^ ((2 * b + d) & 7)) for k2, d in pairs])
+    return out
+
+
 def conflict_ratio(info, esize):
-    if info["kernel"] == _native.SFFT_KERNEL_STOCKHAM:
+    if info["kernel"] == _native.SFFT_KERNEL_FOURSTEP:
+        instrs = fourstep_instructions(info)
+        unit = esize
+    elif info["kernel"] == _native.SFFT_KERNEL_STOCKHAM:
         instrs = stockham_instructions(info, esize)
         unit = 8 if info["layout"] == 3 else esize
     elif info["kernel"] == _native.SFFT_KERNEL_SPLIT2:
@@ -217,3 +240,16 @@ def test_swizzles_are_bijections():
         for r in rs:
             assert sorted(swz_row(e, r, esize) for e in range(4096)) == list(range(4096))
     assert sorted(swz_chunk(c) for c in range(4096)) == list(range(4096))
+
+
+def test_fourstep_variant_conflict_free():
+    """The four-step kernel's gather, transpose write and transpose read are
+    conflict-free (its radix-2 level moves through shuffles, not shared memory)."""
+    lib = _native.lib()
+    seen = 0
+    for v in range(lib.sfft_num_variants(2048, 1)):
+        info = _native.variant_info(2048, 1, v)
+        if info["kernel"] == _native.SFFT_KERNEL_FOURSTEP:
+            assert conflict_ratio(info, 16) == 1.0
+            seen += 1
+    assert seen >= 1

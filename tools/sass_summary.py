@@ -117,6 +117,10 @@ def classify(demangled: str, sigs):
         return (f"stockham_tmem {m.group(1)} N={m.group(2)} R={m.group(3)} {'inv' if m.group(4) == '1' else 'fwd'} "
                 f"twp={m.group(5)} minb={m.group(7)} loader={'3' if m.group(8) == '1' else '4'}"
                 f"{' real-in' if m.group(6) == '1' else ''}"), False
+    m = re.search(r"sfft::fourstep_kernel<(float|double), ([01]), ([01]), (\d)>", d)
+    if m:
+        return (f"fourstep {m.group(1)} N=2048 {'inv' if m.group(2) == '1' else 'fwd'} minb={m.group(4)}"
+                f"{' real-in' if m.group(3) == '1' else ''}"), False
     m = re.search(r"sfft::stockham_pipe_kernel<(float|double), (\d+), (\d+), (\d+), ([01])", d)
     if m:
         return (f"stockham_pipe {m.group(1)} N={m.group(2)} R={m.group(3)} seq={m.group(4)} "
