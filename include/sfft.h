@@ -124,7 +124,10 @@ int sfft_plan_twiddles(sfft_plan_t plan, void* host_out, int64_t capacity_bytes)
  * `stream` is a cudaStream_t (NULL = legacy default stream).  If
  * `d_nonfinite` is non-NULL the kernel ORs 1 into it when any input value is
  * NaN/Inf (the caller zeroes it and reads it after the stream completes).
- * Alignment: 16 bytes for both pointers. */
+ * Alignment: 16 bytes for both pointers.  Buffers are either disjoint or
+ * identical (complex input in place); any other overlap -- a shifted view,
+ * or real input (_ex) sharing memory with its complex output -- returns
+ * SFFT_ERR_ARGUMENT (the same rule holds for every execute entry point). */
 int sfft_execute(sfft_plan_t plan, const void* d_in, void* d_out, int64_t batch, void* stream,
                  int32_t* d_nonfinite);
 

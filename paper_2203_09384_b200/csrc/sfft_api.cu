@@ -483,6 +483,23 @@ int sfft_plan_twiddles(sfft_plan_t p, void* host_out, int64_t capacity) {
 }
 
 namespace {
+// Input and output may be the same buffer (complex input, in place: every
+// kernel reads its rows before writing them) or disjoint.  Any other overlap
+// -- a shifted view, or real input under its complex output (output row r
+// covers real rows 2r and 2r+1, which other CTAs / later pipeline chunks have
+// not read yet) -- would race, so it is refused.
+bool overlap_refused(const sfft_plan* p, const void* in, const void* out, int64_t batch, int32_t input_kind) {
+  const int64_t row = int64_t(p->n) * (p->precision == SFFT_SINGLE ? 8 : 16);
+  const int64_t in_row = input_kind == SFFT_INPUT_REAL ? row / 2 : row;
+  const uintptr_t i0 = reinterpret_cast<uintptr_t>(in), o0 = reinterpret_cast<uintptr_t>(out);
+  const bool overlap = i0 < o0 + uintptr_t(batch * row) && o0 < i0 + uintptr_t(batch * in_row);
+  if (!overlap) return false;
+  if (i0 == o0 && input_kind == SFFT_INPUT_COMPLEX) return false;
+  fail(SFFT_ERR_ARGUMENT,
+       "input and output overlap: only an identical complex input/output buffer runs in place");
+  return true;
+}
+
 // the kernel for (plan, input kind), or nullptr with the error recorded
 LaunchFn pick_launch(sfft_plan_t p, int32_t input_kind, const void* d_in, const void* d_out, int* rc) {
   *rc = SFFT_OK;
@@ -517,6 +534,7 @@ int sfft_execute_ex(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch,
   int rc = SFFT_OK;
   const LaunchFn launch = pick_launch(p, input_kind, d_in, d_out, &rc);
   if (launch == nullptr) return rc;
+  if (overlap_refused(p, d_in, d_out, batch, input_kind)) return SFFT_ERR_ARGUMENT;
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   const cudaError_t e = launch(d_in, d_out, p->d_tw, batch, reinterpret_cast<int*>(d_nonfinite),
@@ -540,6 +558,7 @@ int sfft_execute_sync_ex(sfft_plan_t p, const void* d_in, void* d_out, int64_t b
   int rc = SFFT_OK;
   const LaunchFn launch = pick_launch(p, input_kind, d_in, d_out, &rc);
   if (launch == nullptr) return rc;
+  if (overlap_refused(p, d_in, d_out, batch, input_kind)) return SFFT_ERR_ARGUMENT;
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   cudaError_t e = t_sync.flag();
@@ -582,6 +601,7 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   const LaunchFn launch = real ? p->v->launch_real[p->direction] : p->v->launch[p->direction];
   if (launch == nullptr)
     return fail(SFFT_ERR_ARGUMENT, "this plan's kernel has no real-input path (see sfft_plan_info.real_input)");
+  if (overlap_refused(p, h_in, h_out, batch, input_kind)) return SFFT_ERR_ARGUMENT;
   HostPipeline& hp = host_pipeline(p->device);
   std::lock_guard<std::mutex> lock(hp.mu);
   DeviceGuard guard(p->device);

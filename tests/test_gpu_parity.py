@@ -262,6 +262,42 @@ def test_misaligned_real_view(cuda, n, prec, offset):
     assert torch.equal(sf.execute(plan, view), want)  # no sticky fault
 
 
+@pytest.mark.parametrize("n,prec", [(8, "single"), (1024, "single"), (2048, "double")])
+def test_overlapping_buffers(cuda, n, prec):
+    """Input and output are disjoint or identical (complex in place).  Real
+    rows under their own complex output, or a shifted complex view, would
+    race between CTAs / pipeline chunks: every entry point refuses them with
+    SFFT_ERR_ARGUMENT, and exact in-place stays bit-identical to out of place."""
+    rows = 33
+    cdt = torch.complex64 if prec == "single" else torch.complex128
+    plan = sf.make_plan(n, precision=prec)
+    x = torch.from_numpy(sf.generate_batch(rows + 1, n, seed=9, precision=prec)).to(cuda)
+    want = sf.execute(plan, x[:rows])
+    # exact in place
+    buf = x[:rows].clone()
+    sf.launch(plan, buf, buf, rows)
+    torch.cuda.synchronize()
+    assert torch.equal(buf, want)
+    # shifted complex view: output one row after the input
+    with pytest.raises(sf.FftError, match="overlap"):
+        sf.launch(plan, x[:rows], x[1:], rows)
+    # real rows inside their complex output buffer (same start address)
+    out = torch.zeros((rows, n), dtype=cdt, device=cuda)
+    real_view = out.view(torch.float32 if prec == "single" else torch.float64).reshape(-1)[: rows * n].reshape(rows, n)
+    assert real_view.data_ptr() == out.data_ptr()
+    with pytest.raises(sf.FftError, match="overlap"):
+        sf.launch(plan, real_view, out, rows)
+    with pytest.raises(sf.FftError, match="overlap"):
+        sf.execute(plan, real_view, out=out)
+    # the host pipeline: a real numpy view of the complex output array
+    hout = np.zeros((rows, n), dtype=dtype_of(prec))
+    hreal = hout.view(np.float32 if prec == "single" else np.float64).reshape(-1)[: rows * n].reshape(rows, n)
+    with pytest.raises(sf.FftError, match="overlap"):
+        sf.execute(plan, hreal, out=hout)
+    torch.cuda.synchronize()
+    assert torch.equal(sf.execute(plan, x[:rows]), want)  # context still usable
+
+
 def test_shared_plan_across_threads(cuda):
     from concurrent.futures import ThreadPoolExecutor
 
