@@ -22,6 +22,9 @@ device time is the max over ranks (one all_reduce of a scalar).
                    roofline fraction, spot parity and clocks per point (N=1 only).
 * ``c4``        -- BASELINE configs[3]: fp64 N=2048, batch 131072 (4 GiB in),
                    with its own roofline and clocks (N=1 only).
+* ``sustained`` -- seconds-long (power-capped) load: torch copy_ vs the
+                   default kernel at configs[1] and fp64 N=2048, GB/s and
+                   clocks of the settled half of each window (N=1 only).
 * ``cpu_baseline`` -- the reference algorithm (oracle/, the batched restatement
                    of stagefft, bit-exact to it) on the host after all GPU
                    timing, rank 0, every N: all cores (headline), one process,
@@ -412,6 +415,53 @@ def run_c4(sf, dev, stream, clocks, peak, launches=20, warmup=3, cool=0.3):
             "clocks": _clock_brief(clocks.summary(t0, t1))}
 
 
+def run_sustained(sf, dev, stream, clocks, peak, secs=3.0, block=25):
+    """Seconds-long load (the power-capped regime): for configs[1] and for
+    fp64 N=2048 (configs[3]'s length, 1 GiB in), torch ``copy_`` of the same
+    buffers -- the memory system's own sustained rate -- then the default
+    kernel, each launched back to back for `secs` seconds in blocks of
+    `block` launches timed with events; the GB/s of the second half of each
+    window (clocks settled) and the clocks of that half are kept."""
+    import torch
+
+    def window(fn, nbytes):
+        rates, marks = [], []
+        t_end = time.perf_counter() + secs
+        while time.perf_counter() < t_end:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            a.record(stream)
+            for _ in range(block):
+                fn()
+            b.record(stream)
+            b.synchronize()
+            rates.append(2 * nbytes * block / (a.elapsed_time(b) * 1e-3) / 1e9)
+            marks.append((t0, time.perf_counter()))
+        h = len(rates) // 2
+        return statistics.median(rates[h:]), _clock_brief(clocks.summary(marks[h][0], marks[-1][1]))
+
+    points = []
+    for n, rows, precision in ((1024, 65536, "single"), (2048, 32768, "double")):
+        cdt = torch.complex64 if precision == "single" else torch.complex128
+        x = torch.empty((rows, n), dtype=cdt, device=dev)
+        torch.view_as_real(x).uniform_(-1.0, 1.0)
+        y = torch.empty_like(x)
+        plan = sf.make_plan(n, "forward", precision=precision)
+        nbytes = rows * row_bytes(n, precision)
+        with torch.cuda.stream(stream):
+            copy_gbs, copy_clk = window(lambda: y.copy_(x), nbytes)
+        fft_gbs, fft_clk = window(lambda: sf.launch(plan, x, y, rows, stream=stream), nbytes)
+        points.append({"precision": precision, "n": n, "batch": rows, "copy_gbs": round(copy_gbs, 1),
+                       "fft_gbs": round(fft_gbs, 1), "fft_over_sustained_copy": round(fft_gbs / copy_gbs, 4),
+                       "fft_over_burst_peak": round(fft_gbs / peak, 4), "copy_clocks": copy_clk,
+                       "fft_clocks": fft_clk})
+        del x, y
+        torch.cuda.empty_cache()
+    return {"workload": f"{secs:g} s back-to-back per leg (torch copy_ of the same buffers, then the default "
+                        "kernel): configs[1] and fp64 N=2048; GB/s of each window's second half",
+            "secs_per_leg": secs, "points": points}
+
+
 # ----------------------------------------------------------------- GPU arm
 def run_gpu(args, n, batch, precision, direction, workload):
     import torch
@@ -615,7 +665,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
     if world == 1 and not args.no_extras:
         # BASELINE configs[2] and [3] under the same clock record as `value`;
         # a failure here (e.g. a smaller device) must not cost the main line
-        for key, fn in (("sweep", run_sweep), ("c4", run_c4)):
+        for key, fn in (("sweep", run_sweep), ("c4", run_c4), ("sustained", run_sustained)):
             try:
                 out[key] = fn(sf, dev, stream, clocks, peak)
             except Exception as exc:  # noqa: BLE001 - reported in the line instead
@@ -695,7 +745,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the sweep (configs[2]) and c4 (configs[3]) keys")
+    ap.add_argument("--no-extras", action="store_true", help="skip the sweep (configs[2]), c4 (configs[3]) and sustained keys")
     ap.add_argument("--fill-hbm", type=float, default=0.0, metavar="FRAC",
                     help="size the batch so input + output take FRAC of free HBM (BASELINE configs[3]); "
                          "the e2e leg then runs on a <= 4 GiB host block")

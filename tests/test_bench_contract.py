@@ -78,6 +78,12 @@ def test_gpu_arm_line(cuda):
     c4 = d["c4"]
     assert c4["roofline"]["algorithmic_bytes_per_launch"] == 2 * 131072 * 2048 * 16
     assert c4["parity_rel_l2_max_vs_numpy_c128"] <= 1e-13 * 11 and c4["value"] > 0
+    sus = d["sustained"]
+    assert [(p["precision"], p["n"]) for p in sus["points"]] == [("single", 1024), ("double", 2048)]
+    for p in sus["points"]:
+        assert p["copy_gbs"] > 0 and p["fft_gbs"] > 0
+        assert abs(p["fft_over_sustained_copy"] - p["fft_gbs"] / p["copy_gbs"]) < 1e-3
+        assert "sm_mhz" in p["fft_clocks"] and "sm_mhz" in p["copy_clocks"]
 
 
 @pytest.mark.gpu
