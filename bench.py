@@ -462,6 +462,34 @@ def run_sustained(sf, dev, stream, clocks, peak, secs=3.0, block=25):
             "secs_per_leg": secs, "points": points}
 
 
+def bind_gpu_local_cpus(device_index: int):
+    """Restrict this process to the CPUs NVML reports as local to the GPU
+    (its NUMA node) before any pinned buffer is allocated, so the e2e leg's
+    staging pages and DMA stay on the GPU's socket -- on a multi-socket,
+    multi-GPU host a rank whose memory lands on the far socket pushes its
+    PCIe traffic across the socket interconnect.  Returns (original CPU set,
+    description); a no-op when the GPU is local to every CPU (one NUMA
+    node, e.g. the 1-GPU lease) or NVML cannot tell."""
+    original = os.sched_getaffinity(0)
+    try:
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(device_index)
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(
+            "%08X:%02X:%02X.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id))
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        local = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+    except Exception as exc:  # noqa: BLE001 - affinity is an optimisation
+        return original, f"unchanged (NVML: {type(exc).__name__})"
+    cpus = local & original
+    if not cpus or cpus == original:
+        return original, f"unchanged (GPU local to all {len(original)} CPUs)"
+    os.sched_setaffinity(0, cpus)
+    return original, f"{len(cpus)} of {len(original)} CPUs (GPU-local NUMA node, NVML)"
+
+
 # ----------------------------------------------------------------- GPU arm
 def run_gpu(args, n, batch, precision, direction, workload):
     import torch
@@ -477,6 +505,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
     backend = os.environ.get("SFFT_BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
+    all_cpus, affinity_note = bind_gpu_local_cpus(local)
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -624,6 +653,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
                           f"input {batch * rb / 2**20:.0f} MiB per GPU fits the {l2_bytes / 2**20:.0f} MiB L2 "
                           "(small test config; not a bench number)"),
             "kernel": {k: info[k] for k in ("kernel", "elems_per_thread", "seqs_per_cta", "threads_per_cta", "radices", "variant")},
+            "host_cpus": affinity_note,
         },
         "e2e": {
             "value": round(e2e_value, 1),
@@ -673,6 +703,7 @@ def run_gpu(args, n, batch, precision, direction, workload):
                 torch.cuda.empty_cache()
     clocks.stop()
     barrier()  # every rank's GPU work is done before rank 0 loads the host
+    os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host core back
     if rank == 0 and not args.no_cpu:
         # rank 0 only, outside every timed region (the other ranks wait below)
         out["cpu_baseline"] = cpu_baseline(n, precision, direction, args.cpu_seconds)
