@@ -720,7 +720,8 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     // Measured (tools/e2e_link_probe.py, profiles/r01_e2e_link.jsonl): 97-99 %
     // of two free-running full-size concurrent copies on the same box; the
     // link, not the pipeline, is the bound.  (Geometric ramp-in/ramp-out
-    // chunk sizes against fill/drain measured no gain.)
+    // chunk sizes against fill/drain measured no gain:
+    // profiles/r02_host_ramp_negative.txt.)
     const unsigned char* src = static_cast<const unsigned char*>(h_in);
     unsigned char* dst = static_cast<unsigned char*>(h_out);
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
