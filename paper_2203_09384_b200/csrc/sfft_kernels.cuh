@@ -548,10 +548,11 @@ __device__ __forceinline__ void pdl_enter() {
 // RIN: the input rows are real (N values of T each, imaginary parts zero) --
 //      the C2C transform of a real signal reads 4 (8) bytes per element
 //      instead of 8 (16) and needs no separate widening pass.
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0, bool RIN = false>
-__global__ void __launch_bounds__((N / R) * SEQ)
-stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
-                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+// The body is shared by stockham_kernel and stockham_kernel_capped (below).
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN>
+__device__ __forceinline__ void stockham_body(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in,
+                                              cx_t<T>* __restrict__ out, const cx_t<T>* __restrict__ tw,
+                                              long long batch, int* __restrict__ nonfinite) {
   using C = cx_t<T>;
   using S = Smem<T, LAYOUT, R>;
   constexpr int G = N / R;
@@ -617,6 +618,23 @@ stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t
                                                   s, valid ? out + seq * N : nullptr, tw);
   if (nonfinite != nullptr && valid && !in_place && j == 0 && !cx_finite(v[0]))
     recheck_row_inputs(in + seq * N, N, nonfinite);
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER = 0, bool RIN = false>
+__global__ void __launch_bounds__((N / R) * SEQ)
+stockham_kernel(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
+                const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  stockham_body<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>(in, out, tw, batch, nonfinite);
+}
+// The same kernel with a minimum of MINB resident CTAs per SM requested from
+// ptxas (a register cap).  A separate kernel because any explicit min-blocks
+// value, 1 included, changes ptxas' allocation (the fp32 N=2048 real-input
+// kernel: 214 registers without, 255 + spills with __launch_bounds__(32, 1)).
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN, int MINB>
+__global__ void __launch_bounds__((N / R) * SEQ, MINB)
+stockham_kernel_capped(const std::conditional_t<RIN, T, cx_t<T>>* __restrict__ in, cx_t<T>* __restrict__ out,
+                       const cx_t<T>* __restrict__ tw, long long batch, int* __restrict__ nonfinite) {
+  stockham_body<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>(in, out, tw, batch, nonfinite);
 }
 
 // LOADER 3 (fp64 N = 2048, R = 16, 128 threads, one sequence per CTA): the

@@ -83,7 +83,16 @@ cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), long long grid, int t
   return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
 }
 
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
+// the Stockham kernel, or its register-capped twin when MINB > 1
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN, int MINB>
+auto stockham_kernel_ptr() {
+  if constexpr (MINB > 1)
+    return sfft::stockham_kernel_capped<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN, MINB>;
+  else
+    return sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>;
+}
+
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false, int MINB = 1>
 cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long batch, int* flag,
                             cudaStream_t st, bool pdl) {
   using C = sfft::cx_t<T>;
@@ -91,12 +100,12 @@ cudaError_t launch_stockham(const void* in, void* out, const void* tw, long long
   constexpr int threads = (N / R) * SEQ;
   constexpr int smem = stockham_smem<T, N, R, SEQ, LAYOUT>();
   const long long grid = (batch + SEQ - 1) / SEQ;
-  return launch_pdl(pdl, sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>, grid, threads, smem,
+  return launch_pdl(pdl, stockham_kernel_ptr<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN, MINB>(), grid, threads, smem,
                     st, static_cast<const In*>(in), static_cast<C*>(out), static_cast<const C*>(tw), batch, flag);
 }
-template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false>
+template <typename T, int N, int R, int SEQ, bool INV, int LAYOUT, int TWP, int LOADER, bool RIN = false, int MINB = 1>
 cudaError_t prepare_stockham(int carveout) {
-  const auto k = sfft::stockham_kernel<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN>;
+  const auto k = stockham_kernel_ptr<T, N, R, SEQ, INV, LAYOUT, TWP, LOADER, RIN, MINB>();
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        stockham_smem<T, N, R, SEQ, LAYOUT>());
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
@@ -175,7 +184,9 @@ cudaError_t prepare_tile(int carveout) {
   return e;
 }
 
-template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0, bool REAL = false>
+// RMINB: min-blocks (register cap) of the real-input instantiations only
+template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0, bool REAL = false,
+          int RMINB = 1>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
@@ -202,10 +213,10 @@ Variant stockham_variant() {
   v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   if constexpr (REAL) {
-    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
-    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
-    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true>;
-    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true>;
+    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true, RMINB>;
+    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true, RMINB>;
+    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true, RMINB>;
+    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true, RMINB>;
   }
   return v;
 }

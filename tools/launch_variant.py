@@ -1,6 +1,8 @@
 """Launch one kernel variant a few times on device-resident rows (ncu target).
 
     python tools/launch_variant.py N precision rows variant [launches]
+
+REAL=1 feeds real rows (the SFFT_INPUT_REAL loader) instead of complex ones.
 """
 import os
 import sys
@@ -15,6 +17,8 @@ launches = int(sys.argv[5]) if len(sys.argv) > 5 else 5
 dt = torch.complex64 if prec == "single" else torch.complex128
 x = torch.randn((rows, n), dtype=dt, device="cuda")
 y = torch.empty_like(x)
+if os.environ.get("REAL") == "1":
+    x = x.real.contiguous()
 plan = sf.make_plan(n, precision=prec, variant=variant)
 for _ in range(launches):
     sf.launch(plan, x, y, rows)

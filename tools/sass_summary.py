@@ -91,14 +91,16 @@ def default_signatures():
 
 def classify(demangled: str, sigs):
     d = re.sub(r"\((?:int|bool)\)", "", demangled)  # cu++filt spells template args as (int)1024, (bool)0
-    m = re.search(r"sfft::stockham_kernel<(float|double), (\d+), (\d+), (\d+), ([01]), (\d), (\d), (\d), ([01])>", d)
+    m = re.search(r"sfft::stockham_kernel(?:_capped)?<(float|double), (\d+), (\d+), (\d+), ([01]), (\d), (\d), (\d), "
+                  r"([01])(?:, (\d+))?>", d)
     if m:
         letter = "f" if m.group(1) == "float" else "d"
         key = ("stockham", letter, int(m.group(2)), int(m.group(3)), int(m.group(4)), int(m.group(6)),
                int(m.group(7)), int(m.group(8)))
         label = (f"stockham {m.group(1)} N={m.group(2)} R={m.group(3)} seq={m.group(4)} "
                  f"{'inv' if m.group(5) == '1' else 'fwd'} layout={m.group(6)} twp={m.group(7)} "
-                 f"loader={m.group(8)}{' real-in' if m.group(9) == '1' else ''}")
+                 f"loader={m.group(8)}{' real-in' if m.group(9) == '1' else ''}"
+                 f"{' minb=' + m.group(10) if m.group(10) else ''}")
         return label, key in sigs
     m = re.search(r"sfft::tile_kernel<(float|double), (\d+), (\d+), (\d+), ([01]), ([01])>", d)
     if m:
