@@ -81,6 +81,8 @@ typedef struct sfft_plan_info {
   int32_t smem_carveout;       /* preferred shared-memory carveout, % of max (-1: driver default) */
   int32_t pipeline_stages;     /* loader 2: shared-memory stage buffers per CTA (else 0) */
   int32_t real_input;          /* 1: SFFT_INPUT_REAL is supported (sfft_execute_ex) */
+  int32_t real_loader;         /* loader of the real-input kernel (same passes, so the same
+                                  results as widening; the loader may differ) */
 } sfft_plan_info_t;
 
 /* Library version (major*10000 + minor*100 + patch). */

@@ -69,6 +69,7 @@ class PlanInfo(ctypes.Structure):
         ("smem_carveout", ctypes.c_int32),
         ("pipeline_stages", ctypes.c_int32),
         ("real_input", ctypes.c_int32),
+        ("real_loader", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

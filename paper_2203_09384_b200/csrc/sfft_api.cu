@@ -392,8 +392,8 @@ int sfft_plan_create_variant(sfft_plan_t* out, int32_t n, int32_t precision, int
     }
   }
   e = p->v->prepare[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
-  if (e == cudaSuccess && p->v->prepare_real[direction])  // same loader, same carveout rule
-    e = p->v->prepare_real[direction](carveout_override() >= -1 ? carveout_override() : p->v->carveout);
+  if (e == cudaSuccess && p->v->prepare_real[direction])  // the real loader's own carveout rule
+    e = p->v->prepare_real[direction](carveout_override() >= -1 ? carveout_override() : p->v->real_carveout);
   if (e != cudaSuccess) {
     cudaFree(p->d_tw);
     delete p;
@@ -441,6 +441,7 @@ int sfft_plan_info(sfft_plan_t p, sfft_plan_info_t* info) {
   info->smem_carveout = carveout_override() >= -1 ? carveout_override() : p->v->carveout;
   info->pipeline_stages = p->v->stages;
   info->real_input = p->v->launch_real[0] != nullptr;
+  info->real_loader = p->v->real_loader;
   return SFFT_OK;
 }
 
@@ -471,6 +472,7 @@ int sfft_variant_info(int32_t n, int32_t precision, int32_t variant, sfft_plan_i
   info->smem_carveout = v.carveout;
   info->pipeline_stages = v.stages;
   info->real_input = v.launch_real[0] != nullptr;
+  info->real_loader = v.real_loader;
   return SFFT_OK;
 }
 

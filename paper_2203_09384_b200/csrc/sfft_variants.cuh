@@ -41,10 +41,13 @@ struct Variant {
   int tw_len;      // per-pass twiddle elements
   LaunchFn launch[2];    // [direction]
   PrepareFn prepare[2];  // [direction]
-  // real-valued input rows (imaginary parts zero), default variants only;
-  // same loader and carveout as the complex kernel
+  // real-valued input rows (imaginary parts zero), default variants only.
+  // Same passes (hence the same arithmetic: bit-identical to widening); the
+  // loader may differ (real_loader), with its own carveout rule.
   LaunchFn launch_real[2];
   PrepareFn prepare_real[2];
+  int real_loader;
+  int real_carveout;
 };
 
 // ---------------------------------------------------------------- launchers
@@ -184,9 +187,11 @@ cudaError_t prepare_tile(int carveout) {
   return e;
 }
 
-// RMINB: min-blocks (register cap) of the real-input instantiations only
+// RMINB: min-blocks (register cap) of the real-input instantiations only;
+// RLOADER: their loader (the passes, hence the results, are the complex
+// kernel's whatever the loader)
 template <typename T, int N, int R, int SEQ, int LAYOUT = 2, int TWP = 0, int LOADER = 0, bool REAL = false,
-          int RMINB = 1>
+          int RMINB = 1, int RLOADER = LOADER>
 Variant stockham_variant() {
   Variant v{};
   v.kernel = SFFT_KERNEL_STOCKHAM;
@@ -208,15 +213,19 @@ Variant stockham_variant() {
   // memory at half the unified 256 KB keeps >= 124 KB of L1.  Bulk (TMA)
   // copies land in shared memory directly and keep the driver default.
   v.carveout = LOADER == 0 ? 50 : -1;
+  v.real_loader = LOADER;
+  v.real_carveout = v.carveout;
   v.launch[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.launch[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   v.prepare[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER>;
   v.prepare[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER>;
   if constexpr (REAL) {
-    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true, RMINB>;
-    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true, RMINB>;
-    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, LOADER, true, RMINB>;
-    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, LOADER, true, RMINB>;
+    v.launch_real[0] = &launch_stockham<T, N, R, SEQ, false, LAYOUT, TWP, RLOADER, true, RMINB>;
+    v.launch_real[1] = &launch_stockham<T, N, R, SEQ, true, LAYOUT, TWP, RLOADER, true, RMINB>;
+    v.prepare_real[0] = &prepare_stockham<T, N, R, SEQ, false, LAYOUT, TWP, RLOADER, true, RMINB>;
+    v.prepare_real[1] = &prepare_stockham<T, N, R, SEQ, true, LAYOUT, TWP, RLOADER, true, RMINB>;
+    v.real_loader = RLOADER;
+    v.real_carveout = RLOADER == 0 ? 50 : -1;
   }
   return v;
 }
@@ -229,6 +238,8 @@ Variant pipe_variant() {
   v.stages = STAGES;
   v.smem = pipe_smem<T, N, R, SEQ, LAYOUT, STAGES>();
   v.carveout = -1;  // bulk copies land in shared memory; the driver sizes it
+  v.real_loader = v.loader;
+  v.real_carveout = v.carveout;
   v.launch[0] = &launch_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
   v.launch[1] = &launch_stockham_pipe<T, N, R, SEQ, true, LAYOUT, TWP, STAGES>;
   v.prepare[0] = &prepare_stockham_pipe<T, N, R, SEQ, false, LAYOUT, TWP, STAGES>;
@@ -258,6 +269,8 @@ Variant tmem_variant() {
   Variant v = stockham_variant<T, N, R, 1, 2, TWP, 1>();
   v.loader = XCH ? 3 : 4;
   v.carveout = -1;  // the bulk copy lands in shared memory
+  v.real_loader = v.loader;
+  v.real_carveout = v.carveout;
   v.launch[0] = &launch_stockham_tmem<T, N, R, false, TWP, false, MINB, XCH>;
   v.launch[1] = &launch_stockham_tmem<T, N, R, true, TWP, false, MINB, XCH>;
   v.prepare[0] = &prepare_stockham_tmem<T, N, R, false, TWP, false, MINB, XCH>;
@@ -305,6 +318,8 @@ Variant split2_variant() {
   v.seq = 1;
   v.smem = split2_smem<T, N, R, LAYOUT>();
   v.carveout = -1;  // the bulk copy lands in shared memory
+  v.real_loader = v.loader;
+  v.real_carveout = v.carveout;
   v.launch[0] = &launch_split2<T, N, R, false, LAYOUT, TWP>;
   v.launch[1] = &launch_split2<T, N, R, true, LAYOUT, TWP>;
   v.prepare[0] = &prepare_split2<T, N, R, false, LAYOUT, TWP>;
@@ -350,6 +365,8 @@ Variant fourstep_variant() {
   v.twp = 2;
   v.loader = 1;
   v.carveout = -1;  // the bulk copy lands in shared memory
+  v.real_loader = v.loader;
+  v.real_carveout = v.carveout;
   v.threads = 128;
   v.smem = 2048 * int(sizeof(sfft::cx_t<T>));
   v.passes = 2;
@@ -381,6 +398,8 @@ Variant tile_variant() {
   v.radices[0] = N;
   v.tw_len = 0;
   v.carveout = -1;  // cp.async stages through shared memory, not L1 lines
+  v.real_loader = v.loader;
+  v.real_carveout = v.carveout;
   v.launch[0] = &launch_tile<T, N, SPT, W, false>;
   v.launch[1] = &launch_tile<T, N, SPT, W, true>;
   v.prepare[0] = &prepare_tile<T, N, SPT, W, false>;
