@@ -312,15 +312,17 @@ def test_shared_plan_across_threads(cuda):
 
 @pytest.mark.parametrize("prec", PRECS)
 def test_all_kernel_variants(cuda, prec):
-    """Every compiled variant (the tuning space) is correct, not just the default."""
+    """Every compiled variant (the tuning space) is correct, not just the
+    default -- forward and inverse against the exact DFT."""
     lib = sf._native.lib()
     for n in ALL_N:
         nvar = lib.sfft_num_variants(n, 0 if prec == "single" else 1)
         x = sf.generate_batch(333, n, seed=11, precision=prec)
-        want = oracle.direct_dft(x)
-        for v in range(nvar):
-            got = run(sf.make_plan(n, precision=prec, variant=v), x, cuda)
-            assert row_rel_l2(got, want).max() <= tolerance(n, prec), (n, v)
+        for direction in DIRS:
+            want = oracle.direct_dft(x, direction)
+            for v in range(nvar):
+                got = run(sf.make_plan(n, direction, precision=prec, variant=v), x, cuda)
+                assert row_rel_l2(got, want).max() <= tolerance(n, prec), (n, v, direction)
 
 
 @pytest.mark.parametrize("direction", DIRS)
