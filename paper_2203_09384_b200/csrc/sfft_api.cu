@@ -539,8 +539,18 @@ int sfft_execute_ex(sfft_plan_t p, const void* d_in, void* d_out, int64_t batch,
   if (overlap_refused(p, d_in, d_out, batch, input_kind)) return SFFT_ERR_ARGUMENT;
   DeviceGuard guard(p->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  // Programmatic dependent launch overlaps back-to-back eager launches, but
+  // inside a captured CUDA graph its programmatic edges cost more than they
+  // save (fp64 N=2048 x 64 rows: 6.4 vs 3.5 us per replayed call;
+  // tools/graph_probe.py, profiles/r02_graph_probe.txt), so captured
+  // launches use plain stream order.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) != cudaSuccess) {
+    cudaGetLastError();
+    cap = cudaStreamCaptureStatusNone;
+  }
   const cudaError_t e = launch(d_in, d_out, p->d_tw, batch, reinterpret_cast<int*>(d_nonfinite),
-                               static_cast<cudaStream_t>(stream), true);
+                               static_cast<cudaStream_t>(stream), cap == cudaStreamCaptureStatusNone);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SFFT_OK;
 }
