@@ -146,7 +146,19 @@ struct HostPipelineShape {
   // r01_e2e_link.jsonl): 32 MiB chunks, 3 slots in flight
   int slots = 3;
   int64_t chunk_bytes = int64_t(32) << 20;
+  // Mid-size calls are cut into several chunks (>= min_chunk bytes) so
+  // their copies overlap instead of running H2D, kernel and D2H back to
+  // back: pinned calls into 4 (<= 32 MiB) or 8 chunks, pageable ones into 4
+  // (their host copies want >= 4 MiB pieces).  Measured 2-512 MiB
+  // (tools/e2e_size_probe.py, profiles/r02_host_split.txt); SFFT_HOST_SPLIT=1
+  // restores one chunk per 32 MiB.
+  int split = 0;  // 0: the rule above; else that many chunks for every call
+  int64_t min_chunk = int64_t(2) << 20;
   HostPipelineShape() {
+    if (const char* e = std::getenv("SFFT_HOST_SPLIT")) {
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= 64) split = v;
+    }
     if (const char* e = std::getenv("SFFT_HOST_SLOTS")) {
       const int v = std::atoi(e);
       if (v >= 2 && v <= kMaxHostStreams) slots = v;
@@ -642,7 +654,16 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
   // both directions with the kernels of neighbouring chunks.
   // Staging buffers grow on demand, so small calls stay small (and
   // zero-copy calls allocate none).
-  const int64_t chunk_bytes = host_shape().chunk_bytes;
+  // Full 32 MiB chunks for long calls; mid-size calls in several chunks
+  // (HostPipelineShape).  The pinned check only matters for copy-engine calls.
+  const bool pinned = total > kSmallCallBytes && is_pinned(h_in) && is_pinned(h_out);
+  int64_t chunk_bytes = host_shape().chunk_bytes;
+  {
+    const int split = host_shape().split ? host_shape().split : (pinned && total > (int64_t(32) << 20) ? 8 : 4);
+    const int64_t per = (total + split - 1) / split;
+    const int64_t want = per < host_shape().min_chunk ? host_shape().min_chunk : per;
+    if (want < chunk_bytes) chunk_bytes = want;
+  }
   const int64_t max_chunk_rows = chunk_bytes / row_bytes > 0 ? chunk_bytes / row_bytes : 1;
   const int64_t want_rows = batch < max_chunk_rows ? batch : max_chunk_rows;
   const int64_t chunk_rows = want_rows;  // rows per pipeline chunk of this call
@@ -701,14 +722,14 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     // bounce buffer (a host memcpy is cheaper than the driver's staging)
     e = ensure_slots();
     if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
-    const bool pinned = is_pinned(h_in) && is_pinned(h_out);
-    if (!pinned && hp.h_stage == nullptr) {
+    const bool small_pinned = is_pinned(h_in) && is_pinned(h_out);
+    if (!small_pinned && hp.h_stage == nullptr) {
       e = cudaHostAlloc(reinterpret_cast<void**>(&hp.h_stage), 2 * kSmallCallBytes, cudaHostAllocPortable);
       if (e != cudaSuccess) return cuda_fail(e, "pinned staging allocation");
     }
     const void* src = h_in;
     void* dst = h_out;
-    if (!pinned) {
+    if (!small_pinned) {
       std::memcpy(hp.h_stage, h_in, size_t(total_in));
       src = hp.h_stage;
       dst = hp.h_stage + kSmallCallBytes;
@@ -719,7 +740,7 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     if (e == cudaSuccess) e = cudaMemcpyAsync(dst, hp.d_out[0], size_t(total), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "small-call pipeline");
-    if (!pinned) std::memcpy(h_out, dst, size_t(total));
+    if (!small_pinned) std::memcpy(h_out, dst, size_t(total));
   } else {
     e = ensure_slots();
     if (e != cudaSuccess) return cuda_fail(e, "host staging allocation");
@@ -736,7 +757,6 @@ int sfft_execute_host_ex(sfft_plan_t p, const void* h_in, void* h_out, int64_t b
     // profiles/r02_host_ramp_negative.txt.)
     const unsigned char* src = static_cast<const unsigned char*>(h_in);
     unsigned char* dst = static_cast<unsigned char*>(h_out);
-    const bool pinned = is_pinned(h_in) && is_pinned(h_out);
     const int S = hp.nslots;
     const int64_t stage_bytes = chunk_rows * row_bytes;
     if (!pinned && hp.h_chunk_bytes < stage_bytes) {
