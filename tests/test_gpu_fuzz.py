@@ -8,6 +8,8 @@ persistent-grid tail, offsets into a larger buffer, and rows scaled by 2^-60
 .. 2^60 (the relative tolerance must hold at every scale).
 """
 
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, settings
@@ -38,7 +40,7 @@ def cases(draw):
     }
 
 
-@settings(max_examples=120, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@settings(max_examples=int(os.environ.get("SFFT_FUZZ_EXAMPLES", "120")), deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(cases())
 def test_random_shapes_match_oracle(cuda, c):
     n, prec = c["n"], c["prec"]
@@ -57,7 +59,7 @@ def test_random_shapes_match_oracle(cuda, c):
     assert row_rel_l2(got, want).max() <= tol
 
 
-@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@settings(max_examples=int(os.environ.get("SFFT_FUZZ_EXAMPLES_HOST", "60")), deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(p=st.integers(1, 11), prec=st.sampled_from(["single", "double"]),
        direction=st.sampled_from(["forward", "inverse"]), batch=st.integers(0, 3000),
        pinned=st.booleans(), seed=st.integers(0, 2**31 - 1))
