@@ -159,6 +159,10 @@ struct HostPipelineShape {
       const int v = std::atoi(e);
       if (v >= 1 && v <= 64) split = v;
     }
+    if (const char* e = std::getenv("SFFT_HOST_MIN_CHUNK_KB")) {
+      const long v = std::atol(e);
+      if (v >= 64 && v <= (long(1) << 20)) min_chunk = int64_t(v) << 10;
+    }
     if (const char* e = std::getenv("SFFT_HOST_SLOTS")) {
       const int v = std::atoi(e);
       if (v >= 2 && v <= kMaxHostStreams) slots = v;

@@ -19,7 +19,7 @@ import paper_2203_09384_b200 as sf  # noqa: E402
 
 n = 1024
 plan = sf.make_plan(n)
-for mib in (2, 4, 8, 16, 32, 64, 128, 512):
+for mib in [int(m) for m in os.environ.get("SIZES_MIB", "2,4,8,16,32,64,128,512").split(",")]:
     rows = (mib << 20) // (n * 8)
     for kind in ("pinned", "pageable"):
         if kind == "pinned":
@@ -37,5 +37,5 @@ for mib in (2, 4, 8, 16, 32, 64, 128, 512):
             sf.execute(plan, a, out=b)
             ts.append(time.perf_counter() - t)
         dt = statistics.median(ts)
-        print(json.dumps({"split": os.environ.get("SFFT_HOST_SPLIT", "default"), "mib": mib, "kind": kind,
+        print(json.dumps({"split": os.environ.get("SFFT_HOST_SPLIT", "default"), "min_chunk_kb": os.environ.get("SFFT_HOST_MIN_CHUNK_KB", "2048"), "mib": mib, "kind": kind,
                           "ms": round(dt * 1e3, 3), "gbs_each_way": round(rows * n * 8 / dt / 1e9, 1)}), flush=True)
